@@ -1,0 +1,928 @@
+// iabn.cu -- host side of the C ABI declared in include/iabn.h.
+//
+// Validation (synchronous, before any launch), schedule selection
+// (channel-resident cluster kernels when the per-channel slab fits in the
+// shared memory of a <=16-CTA cluster, else the streaming kernels), launches on
+// the caller's stream, and the NCCL exchange of the synchronized variant
+// (libnccl.so.2 loaded with dlopen, so the library loads without NCCL/GPU).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "iabn.h"
+#include "kernels_fused.cuh"
+#include "kernels_stream.cuh"
+
+using namespace iabn;
+
+// ====================================================================== status / errors
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+iabn_status fail(iabn_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+iabn_status check_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(IABN_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return IABN_OK;
+}
+
+#define IABN_TRY(expr)                        \
+    do {                                      \
+        const iabn_status _s = (expr);        \
+        if (_s != IABN_OK) return _s;         \
+    } while (0)
+
+// ====================================================================== device facts
+struct DevFacts {
+    int sms = 0;
+    int max_smem_optin = 0;
+    bool attrs_set = false;
+};
+constexpr int kMaxDev = 64;
+DevFacts g_dev[kMaxDev];
+std::mutex g_dev_mu;
+
+iabn_status device_facts(DevFacts** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(IABN_ERR_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+    if (dev < 0 || dev >= kMaxDev) return fail(IABN_ERR_CUDA, "device ordinal %d too large", dev);
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevFacts& f = g_dev[dev];
+    if (f.sms == 0) {
+        cudaDeviceGetAttribute(&f.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&f.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (f.sms <= 0) return fail(IABN_ERR_CUDA, "no usable CUDA device");
+    }
+    if (!f.attrs_set) {
+        const int dyn = f.max_smem_optin - 4096;  // leave room for static smem
+        const void* fns[] = {(const void*)fused_fwd_kernel<float>,
+                             (const void*)fused_fwd_kernel<__nv_bfloat16>,
+                             (const void*)fused_bwd_kernel<float>,
+                             (const void*)fused_bwd_kernel<__nv_bfloat16>};
+        for (const void* fn : fns) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
+        e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return fail(IABN_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e));
+        f.attrs_set = true;
+    }
+    *out = &f;
+    return IABN_OK;
+}
+
+// ====================================================================== geometry
+struct Geom {
+    int64_t N, C, HW, m, E;
+    int dtype, layout, b;
+};
+
+iabn_status make_geom(const iabn_desc* d, Geom* g) {
+    if (!d) return fail(IABN_ERR_INVALID_ARG, "desc is NULL");
+    if (d->n <= 0 || d->c <= 0 || d->hw <= 0)
+        return fail(IABN_ERR_INVALID_ARG, "empty input: n=%lld c=%lld hw=%lld", (long long)d->n,
+                    (long long)d->c, (long long)d->hw);
+    if (d->dtype != IABN_F32 && d->dtype != IABN_BF16)
+        return fail(IABN_ERR_UNSUPPORTED, "unknown dtype %d", d->dtype);
+    if (d->layout != IABN_NCHW && d->layout != IABN_NHWC)
+        return fail(IABN_ERR_UNSUPPORTED, "unknown layout %d", d->layout);
+    g->N = d->n;
+    g->C = d->c;
+    g->HW = d->hw;
+    if (g->N > (1ll << 31) / g->HW)
+        return fail(IABN_ERR_UNSUPPORTED, "n*hw = %lld values per channel exceeds 2^31",
+                    (long long)(g->N * g->HW));
+    g->m = g->N * g->HW;
+    if (g->C > (1ll << 31) / g->HW)
+        return fail(IABN_ERR_UNSUPPORTED, "c*hw exceeds 2^31 (one sample too large)");
+    if (g->C > (1ll << 40) / g->m) return fail(IABN_ERR_UNSUPPORTED, "tensor too large");
+    g->E = g->m * g->C;
+    g->dtype = d->dtype;
+    g->layout = d->layout;
+    g->b = d->dtype == IABN_F32 ? 4 : 2;
+    return IABN_OK;
+}
+
+bool vec_ok(const Geom& g) {
+    return g.layout == IABN_NCHW ? (g.HW * g.b) % 16 == 0 : (g.C * g.b) % 16 == 0;
+}
+
+// Split count of the streaming reductions: independent of the device so that
+// workspace sizes and reduction trees (hence results) are fixed per shape.
+constexpr int64_t kTargetCtas = 148 * 8;
+int stat_splits(const Geom& g) {
+    const int64_t target = kTargetCtas;
+    int64_t units, per_unit_min, work;
+    if (g.layout == IABN_NCHW) {
+        units = g.C;
+        work = g.m;
+        per_unit_min = 4096;
+    } else {
+        const int64_t V = vec_ok(g) ? 16 / g.b : 1;
+        units = (g.C + 16 * V - 1) / (16 * V);
+        work = g.m;  // rows
+        per_unit_min = 16 * 16;
+    }
+    int64_t S = (target + units - 1) / units;
+    S = std::min<int64_t>(S, std::max<int64_t>(1, work / per_unit_min));
+    S = std::max<int64_t>(1, std::min<int64_t>(S, 65535));
+    return (int)S;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct WsLayout {
+    size_t part, stats, sums_loc, sums_glob, coef, total;
+};
+WsLayout ws_layout(const Geom& g, int S) {
+    WsLayout w;
+    size_t off = 0;
+    w.part = off;
+    off += align256((size_t)S * g.C * 3 * sizeof(double));
+    w.stats = off;
+    off += align256((size_t)g.C * 3 * sizeof(double));
+    w.sums_loc = off;
+    off += align256((size_t)(2 * g.C + 1) * sizeof(double));
+    w.sums_glob = off;
+    off += align256((size_t)(2 * g.C + 1) * sizeof(double));
+    w.coef = off;
+    off += align256((size_t)g.C * sizeof(float4));
+    w.total = off;
+    return w;
+}
+
+// ====================================================================== argument checks
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+iabn_status check_scalars(float eps, float slope) {
+    if (!(eps > 0.f) || !std::isfinite(eps))
+        return fail(IABN_ERR_INVALID_ARG, "eps must be finite and > 0 (got %g)", (double)eps);
+    if (!(slope > 0.f && slope <= 1.f))
+        return fail(IABN_ERR_INVALID_ARG, "slope must be in (0, 1] (got %g)", (double)slope);
+    return IABN_OK;
+}
+
+iabn_status check_momentum(float momentum) {
+    if (!(momentum >= 0.f && momentum <= 1.f))
+        return fail(IABN_ERR_INVALID_ARG, "momentum must be in [0, 1] (got %g)", (double)momentum);
+    return IABN_OK;
+}
+
+iabn_status check_act(const char* name, const void* p) {
+    if (!p) return fail(IABN_ERR_INVALID_ARG, "%s is NULL", name);
+    if (!aligned16(p))
+        return fail(IABN_ERR_UNSUPPORTED, "%s is not 16-byte aligned", name);
+    return IABN_OK;
+}
+
+// a and b must be equal or disjoint ranges of `bytes`
+iabn_status check_same_or_disjoint(const char* an, const void* a, const char* bn, const void* b,
+                                   size_t bytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    if (x == y) return IABN_OK;
+    if (x < y + bytes && y < x + bytes)
+        return fail(IABN_ERR_ALIAS, "%s and %s partially overlap", an, bn);
+    return IABN_OK;
+}
+iabn_status check_disjoint(const char* an, const void* a, const char* bn, const void* b,
+                           size_t bytes) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    if (x < y + bytes && y < x + bytes) return fail(IABN_ERR_ALIAS, "%s and %s overlap", an, bn);
+    return IABN_OK;
+}
+
+iabn_status check_ws(const Geom& g, void* ws, size_t ws_bytes, const WsLayout& w) {
+    if (!ws) return fail(IABN_ERR_WORKSPACE, "workspace is NULL");
+    if (!aligned16(ws)) return fail(IABN_ERR_WORKSPACE, "workspace not 16-byte aligned");
+    if (ws_bytes < w.total)
+        return fail(IABN_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, w.total);
+    (void)g;
+    return IABN_OK;
+}
+
+// ====================================================================== fused planning
+size_t fused_budget_bytes() {
+    static size_t budget = [] {
+        const char* s = getenv("IABN_FUSED_SMEM_KB");
+        const long kb = s ? atol(s) : 100;
+        return (size_t)(kb > 0 ? kb : 100) * 1024;
+    }();
+    return budget;
+}
+
+struct FusedPlan {
+    bool ok = false;
+    int K = 0;
+    uint32_t chunk_vecs = 0;
+    size_t smem = 0;
+};
+
+FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
+    FusedPlan p;
+    if (g.layout != IABN_NCHW || (g.HW * g.b) % 16 != 0) return p;
+    const int nin = pass == 0 ? 1 : 2;
+    const int64_t mv = g.m * g.b / 16;
+    const size_t budget = std::min<size_t>(fused_budget_bytes(), (size_t)f.max_smem_optin - 4096);
+    for (int K = 1; K <= 16 && K <= mv; ++K) {
+        const int64_t per = (mv + K - 1) / K;
+        const size_t bytes = (size_t)per * 16 * nin;
+        if (bytes <= budget) {
+            p.K = K;
+            p.smem = bytes;
+            const int64_t cv = std::max<int64_t>(512 / nin, (per + kMaxChunks - 1) / kMaxChunks);
+            p.chunk_vecs = (uint32_t)cv;
+            p.ok = true;
+            break;
+        }
+    }
+    if (!p.ok) return p;
+    // the cluster must be schedulable (K CTAs with this much shared memory)
+    static std::mutex mu;
+    static int cache_key[64][2][2][17];
+    static int cache_val[64][2][2][17];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int di = dev & 63, ti = g.dtype;
+    std::lock_guard<std::mutex> lk(mu);
+    int& key = cache_key[di][pass][ti][p.K];
+    int& val = cache_val[di][pass][ti][p.K];
+    const int want = (int)((p.smem + 1023) / 1024);
+    if (key < want || key == 0) {  // probe (monotone in smem)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(p.K * 2), 1, 1);
+        cfg.blockDim = dim3(kThreads, 1, 1);
+        cfg.dynamicSmemBytes = p.smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = p.K;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        const void* fn = pass == 0 ? (g.dtype == IABN_F32 ? (const void*)fused_fwd_kernel<float>
+                                                          : (const void*)fused_fwd_kernel<__nv_bfloat16>)
+                                   : (g.dtype == IABN_F32 ? (const void*)fused_bwd_kernel<float>
+                                                          : (const void*)fused_bwd_kernel<__nv_bfloat16>);
+        const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        key = want;
+        val = n;
+    }
+    if (val <= 0) p.ok = false;
+    return p;
+}
+
+FastDiv fd32(int64_t d) { return make_fastdiv((uint32_t)d); }
+
+template <typename T>
+iabn_status launch_fused(int pass, const FusedPlan& p, const FusedArgs& a, int64_t C,
+                         cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(C * p.K), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (pass == 0)
+        e = cudaLaunchKernelEx(&cfg, fused_fwd_kernel<T>, a);
+    else
+        e = cudaLaunchKernelEx(&cfg, fused_bwd_kernel<T>, a);
+    if (e != cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return fail(IABN_ERR_CUDA, "fused launch: %s", cudaGetErrorString(e));
+    }
+    return check_launch(pass == 0 ? "fused_fwd_kernel" : "fused_bwd_kernel");
+}
+
+// ====================================================================== streaming launches
+template <typename T>
+iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cudaStream_t st) {
+    const bool vec = vec_ok(g);
+    if (g.layout == IABN_NCHW) {
+        const dim3 grid((unsigned)g.C, (unsigned)S);
+        const FastDiv fd = fd32(g.HW);
+        if (vec)
+            stats_nchw_kernel<T, true><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.HW,
+                                                                  (uint32_t)g.m, fd, part);
+        else
+            stats_nchw_kernel<T, false><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.HW,
+                                                                   (uint32_t)g.m, fd, part);
+    } else {
+        const int V = vec ? 16 / g.b : 1;
+        const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
+        if (vec)
+            stats_nhwc_kernel<T, true><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.m, part);
+        else
+            stats_nhwc_kernel<T, false><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.m, part);
+    }
+    return check_launch("stats kernel");
+}
+
+template <typename T>
+iabn_status launch_bwd_reduce(const Geom& g, int S, const void* z, const void* dz,
+                              const float* gamma, const float* beta, float eps, float slope,
+                              uint32_t flags, double* part, cudaStream_t st) {
+    const bool vec = vec_ok(g);
+    const float inv_slope = 1.0f / slope;
+    if (g.layout == IABN_NCHW) {
+        const dim3 grid((unsigned)g.C, (unsigned)S);
+        const FastDiv fd = fd32(g.HW);
+        if (vec)
+            bwd_reduce_nchw_kernel<T, true><<<grid, kThreads, 0, st>>>(
+                (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, (uint32_t)g.m, fd, eps, slope,
+                inv_slope, flags, part);
+        else
+            bwd_reduce_nchw_kernel<T, false><<<grid, kThreads, 0, st>>>(
+                (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, (uint32_t)g.m, fd, eps, slope,
+                inv_slope, flags, part);
+    } else {
+        const int V = vec ? 16 / g.b : 1;
+        const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
+        if (vec)
+            bwd_reduce_nhwc_kernel<T, true><<<grid, kThreads, 0, st>>>(
+                (const T*)z, (const T*)dz, gamma, beta, g.C, g.m, eps, slope, inv_slope, flags,
+                part);
+        else
+            bwd_reduce_nhwc_kernel<T, false><<<grid, kThreads, 0, st>>>(
+                (const T*)z, (const T*)dz, gamma, beta, g.C, g.m, eps, slope, inv_slope, flags,
+                part);
+    }
+    return check_launch("bwd_reduce kernel");
+}
+
+// Elementwise passes in whole-sample chunks of < 2^31 elements whose byte
+// offsets stay 16-byte aligned (channel phase is preserved at sample boundaries).
+int64_t samples_per_chunk(const Geom& g) {
+    const int64_t per = g.C * g.HW;
+    int64_t spc = ((1ll << 31) - 1) / per;
+    int64_t q = 1;
+    while (q < 16 && ((per * g.b * q) % 16) != 0) q *= 2;
+    spc = (spc / q) * q;
+    return spc;
+}
+
+int apply_grid(int64_t E, int b, int sms) {
+    const int64_t nvec = E * b / 16;
+    const int64_t want = (nvec + (int64_t)kThreads * kUnroll - 1) / ((int64_t)kThreads * kUnroll);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
+}
+
+template <typename T>
+iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4* coef,
+                             float slope, int sms, cudaStream_t st) {
+    const int64_t spc = samples_per_chunk(g);
+    if (spc <= 0) return fail(IABN_ERR_UNSUPPORTED, "sample too large for the streaming apply");
+    const bool al = vec_ok(g);
+    const FastDiv fh = fd32(g.HW), fc = fd32(g.C);
+    for (int64_t n0 = 0; n0 < g.N; n0 += spc) {
+        const int64_t nn = std::min(spc, g.N - n0);
+        const int64_t off = n0 * g.C * g.HW;
+        const uint32_t E = (uint32_t)(nn * g.C * g.HW);
+        const T* xp = (const T*)x + off;
+        T* zp = (T*)z + off;
+        const int grid = apply_grid(E, g.b, sms);
+        if (g.layout == IABN_NCHW) {
+            if (al)
+                fwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+            else
+                fwd_apply_kernel<T, 0, false><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+        } else {
+            if (al)
+                fwd_apply_kernel<T, 1, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+            else
+                fwd_apply_kernel<T, 1, false><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+        }
+        IABN_TRY(check_launch("fwd_apply kernel"));
+    }
+    return IABN_OK;
+}
+
+template <typename T>
+iabn_status launch_bwd_apply(const Geom& g, const void* z, const void* dz, void* dx,
+                             const float4* coef, float slope, int sms, cudaStream_t st) {
+    const int64_t spc = samples_per_chunk(g);
+    if (spc <= 0) return fail(IABN_ERR_UNSUPPORTED, "sample too large for the streaming apply");
+    const bool al = vec_ok(g);
+    const FastDiv fh = fd32(g.HW), fc = fd32(g.C);
+    const float inv_slope = 1.0f / slope;
+    for (int64_t n0 = 0; n0 < g.N; n0 += spc) {
+        const int64_t nn = std::min(spc, g.N - n0);
+        const int64_t off = n0 * g.C * g.HW;
+        const uint32_t E = (uint32_t)(nn * g.C * g.HW);
+        const T* zp = (const T*)z + off;
+        const T* dzp = (const T*)dz + off;
+        T* dxp = (T*)dx + off;
+        const int grid = apply_grid(E, g.b, sms);
+        if (g.layout == IABN_NCHW) {
+            if (al)
+                bwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+            else
+                bwd_apply_kernel<T, 0, false><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+        } else {
+            if (al)
+                bwd_apply_kernel<T, 1, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+            else
+                bwd_apply_kernel<T, 1, false><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+        }
+        IABN_TRY(check_launch("bwd_apply kernel"));
+    }
+    return IABN_OK;
+}
+
+unsigned cgrid(int64_t C) { return (unsigned)((C + 127) / 128); }
+
+// ====================================================================== NCCL (dlopen)
+struct Nccl {
+    bool tried = false, ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+Nccl* nccl() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!g_nccl.tried) {
+        g_nccl.tried = true;
+        const char* env = getenv("IABN_NCCL_LIB");
+        void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            g_nccl.why = dlerror();
+        } else {
+            g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+            g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+            g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+            g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+            g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+            g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce &&
+                        g_nccl.CommDestroy && g_nccl.GetErrorString;
+            if (!g_nccl.ok) g_nccl.why = "libnccl.so.2 lacks required symbols";
+        }
+    }
+    return g_nccl.ok ? &g_nccl : nullptr;
+}
+
+}  // namespace
+
+struct iabn_comm_s {
+    ncclComm_t comm;
+    int nranks, rank;
+};
+
+namespace {
+
+iabn_status allreduce_f64(double* buf, size_t count, iabn_comm comm, cudaStream_t st) {
+    Nccl* n = nccl();
+    if (!n) return fail(IABN_ERR_NCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+    const ncclResult_t r = n->AllReduce(buf, buf, count, ncclFloat64, ncclSum, comm->comm, st);
+    if (r != ncclSuccess) return fail(IABN_ERR_NCCL, "ncclAllReduce: %s", n->GetErrorString(r));
+    return IABN_OK;
+}
+
+// ====================================================================== shared call bodies
+struct Ctx {
+    Geom g;
+    DevFacts* dev;
+    int S;
+    WsLayout w;
+    unsigned char* ws;
+    cudaStream_t st;
+};
+
+// Host-only part of a call: geometry and workspace (no device access, so the
+// validation paths run without a GPU).
+iabn_status make_ctx(const iabn_desc* desc, void* ws, size_t ws_bytes, void* stream, Ctx* c) {
+    IABN_TRY(make_geom(desc, &c->g));
+    c->dev = nullptr;
+    c->S = stat_splits(c->g);
+    c->w = ws_layout(c->g, c->S);
+    IABN_TRY(check_ws(c->g, ws, ws_bytes, c->w));
+    c->ws = (unsigned char*)ws;
+    c->st = (cudaStream_t)stream;
+    return IABN_OK;
+}
+
+iabn_status attach_device(Ctx& c) { return device_facts(&c.dev); }
+
+template <typename T>
+T* wsp(const Ctx& c, size_t off) {
+    return (T*)(c.ws + off);
+}
+
+iabn_status validate_fwd(const Ctx& c, const void* x, void* z, const float* gamma,
+                         const float* beta, float* rm, float* rv, float* sm, float* sv,
+                         float momentum, float eps, float slope, uint32_t flags, int64_t m_global) {
+    IABN_TRY(check_act("x", x));
+    IABN_TRY(check_act("z", z));
+    IABN_TRY(check_same_or_disjoint("x", x, "z", z, (size_t)c.g.E * c.g.b));
+    if (!gamma || !beta) return fail(IABN_ERR_INVALID_ARG, "gamma/beta is NULL");
+    IABN_TRY(check_scalars(eps, slope));
+    if (flags & IABN_EVAL) {
+        if (!rm || !rv) return fail(IABN_ERR_INVALID_ARG, "eval mode needs running_mean/var");
+        return IABN_OK;
+    }
+    IABN_TRY(check_momentum(momentum));
+    if (!sm || !sv) return fail(IABN_ERR_INVALID_ARG, "save_mean/save_var is NULL");
+    if ((rm == nullptr) != (rv == nullptr))
+        return fail(IABN_ERR_INVALID_ARG, "running_mean and running_var must both be given or both NULL");
+    if (m_global < 2)
+        return fail(IABN_ERR_DEGENERATE, "training needs >= 2 values per channel (got %lld)",
+                    (long long)m_global);
+    return IABN_OK;
+}
+
+iabn_status validate_bwd(const Ctx& c, const void* z, const void* dz, void* dx,
+                         const float* gamma, const float* beta, const float* sv, float* dg,
+                         float* db, float eps, float slope) {
+    IABN_TRY(check_act("z", z));
+    IABN_TRY(check_act("dz", dz));
+    IABN_TRY(check_act("dx", dx));
+    const size_t bytes = (size_t)c.g.E * c.g.b;
+    IABN_TRY(check_same_or_disjoint("dz", dz, "dx", dx, bytes));
+    IABN_TRY(check_disjoint("z", z, "dx", dx, bytes));
+    if (!gamma || !beta || !sv || !dg || !db)
+        return fail(IABN_ERR_INVALID_ARG, "gamma/beta/save_var/dgamma/dbeta is NULL");
+    IABN_TRY(check_scalars(eps, slope));
+    return IABN_OK;
+}
+
+template <typename T>
+iabn_status fwd_stream_stats(const Ctx& c, const void* x) {
+    return launch_stats<T>(c.g, c.S, x, wsp<double>(c, c.w.part), c.st);
+}
+
+template <typename T>
+iabn_status fwd_from_partials(const Ctx& c, const double* part, int S, const void* x, void* z,
+                              const float* gamma, const float* beta, float* rm, float* rv,
+                              float* sm, float* sv, float momentum, float eps, float slope,
+                              uint32_t flags) {
+    FwdCoefArgs a{part, S, c.g.C, gamma, beta, rm, rv, sm, sv, wsp<float4>(c, c.w.coef),
+                  momentum, eps, flags};
+    fwd_coef_kernel<<<cgrid(c.g.C), 128, 0, c.st>>>(a);
+    IABN_TRY(check_launch("fwd_coef kernel"));
+    return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
+}
+
+template <typename T>
+iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamma,
+                         const float* beta, float* rm, float* rv, float* sm, float* sv,
+                         float momentum, float eps, float slope, uint32_t flags) {
+    if (flags & IABN_EVAL) {
+        eval_coef_kernel<<<cgrid(c.g.C), 128, 0, c.st>>>(c.g.C, gamma, beta, rm, rv, eps, flags,
+                                                         wsp<float4>(c, c.w.coef));
+        IABN_TRY(check_launch("eval_coef kernel"));
+        return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
+    }
+    FusedPlan p;
+    if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 0, *c.dev);
+    if ((flags & IABN_FORCE_FUSED) && !p.ok)
+        return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shape");
+    if (p.ok) {
+        FusedArgs a{};
+        a.in0 = x;
+        a.out = z;
+        a.gamma = gamma;
+        a.beta = beta;
+        a.running_mean = rm;
+        a.running_var = rv;
+        a.save_mean = sm;
+        a.save_var = sv;
+        a.C = c.g.C;
+        a.HW = c.g.HW;
+        a.m = (uint32_t)c.g.m;
+        a.fd_hw = fd32(c.g.HW);
+        a.chunk_vecs = p.chunk_vecs;
+        a.momentum = momentum;
+        a.eps = eps;
+        a.slope = slope;
+        a.inv_slope = 1.0f / slope;
+        a.flags = flags;
+        return launch_fused<T>(0, p, a, c.g.C, c.st);
+    }
+    IABN_TRY(fwd_stream_stats<T>(c, x));
+    return fwd_from_partials<T>(c, wsp<double>(c, c.w.part), c.S, x, z, gamma, beta, rm, rv, sm,
+                                sv, momentum, eps, slope, flags);
+}
+
+template <typename T>
+iabn_status bwd_from_sums(const Ctx& c, const double* glob, int Sg, const double* loc, int Sl,
+                          const double* count_ptr, double count, const void* z, const void* dz,
+                          void* dx, const float* gamma, const float* beta, const float* sv,
+                          float* dg, float* db, float eps, float slope, uint32_t flags) {
+    BwdCoefArgs a{glob, Sg, loc, Sl, count_ptr, count, c.g.C, gamma, beta, sv, dg, db,
+                  wsp<float4>(c, c.w.coef), eps, flags};
+    bwd_coef_kernel<<<cgrid(c.g.C), 128, 0, c.st>>>(a);
+    IABN_TRY(check_launch("bwd_coef kernel"));
+    return launch_bwd_apply<T>(c.g, z, dz, dx, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
+}
+
+template <typename T>
+iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
+                          const float* gamma, const float* beta, const float* sv, float* dg,
+                          float* db, float eps, float slope, uint32_t flags) {
+    FusedPlan p;
+    if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 1, *c.dev);
+    if ((flags & IABN_FORCE_FUSED) && !p.ok)
+        return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shape");
+    if (p.ok) {
+        FusedArgs a{};
+        a.in0 = z;
+        a.in1 = dz;
+        a.out = dx;
+        a.gamma = gamma;
+        a.beta = beta;
+        a.save_var = const_cast<float*>(sv);
+        a.dgamma = dg;
+        a.dbeta = db;
+        a.C = c.g.C;
+        a.HW = c.g.HW;
+        a.m = (uint32_t)c.g.m;
+        a.fd_hw = fd32(c.g.HW);
+        a.chunk_vecs = p.chunk_vecs;
+        a.eps = eps;
+        a.slope = slope;
+        a.inv_slope = 1.0f / slope;
+        a.flags = flags;
+        return launch_fused<T>(1, p, a, c.g.C, c.st);
+    }
+    double* part = wsp<double>(c, c.w.part);
+    IABN_TRY(launch_bwd_reduce<T>(c.g, c.S, z, dz, gamma, beta, eps, slope, flags, part, c.st));
+    return bwd_from_sums<T>(c, part, c.S, part, c.S, nullptr, (double)c.g.m, z, dz, dx, gamma,
+                            beta, sv, dg, db, eps, slope, flags);
+}
+
+#define DISPATCH(dtype, fn, ...) \
+    ((dtype) == IABN_F32 ? fn<float>(__VA_ARGS__) : fn<__nv_bfloat16>(__VA_ARGS__))
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int iabn_version(void) { return IABN_VERSION; }
+
+const char* iabn_status_string(iabn_status s) {
+    switch (s) {
+        case IABN_OK: return "IABN_OK";
+        case IABN_ERR_INVALID_ARG: return "IABN_ERR_INVALID_ARG";
+        case IABN_ERR_UNSUPPORTED: return "IABN_ERR_UNSUPPORTED";
+        case IABN_ERR_ALIAS: return "IABN_ERR_ALIAS";
+        case IABN_ERR_DEGENERATE: return "IABN_ERR_DEGENERATE";
+        case IABN_ERR_WORKSPACE: return "IABN_ERR_WORKSPACE";
+        case IABN_ERR_CUDA: return "IABN_ERR_CUDA";
+        case IABN_ERR_NCCL: return "IABN_ERR_NCCL";
+    }
+    return "IABN_ERR_UNKNOWN";
+}
+
+const char* iabn_last_error(void) { return g_err.c_str(); }
+
+uint64_t iabn_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+size_t iabn_workspace_bytes(const iabn_desc* desc) {
+    Geom g;
+    if (make_geom(desc, &g) != IABN_OK) return 0;
+    // splits depend on the SM count; size for the largest B200-class count
+    // without touching the device (callable without a GPU).
+    return ws_layout(g, stat_splits(g)).total;
+}
+
+iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags, int* schedule,
+                                int* cluster) {
+    Geom g;
+    IABN_TRY(make_geom(desc, &g));
+    if (!schedule || !cluster) return fail(IABN_ERR_INVALID_ARG, "NULL output");
+    if (pass != 0 && pass != 1) return fail(IABN_ERR_INVALID_ARG, "pass must be 0 or 1");
+    DevFacts* dev;
+    IABN_TRY(device_facts(&dev));
+    FusedPlan p;
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL))) p = fused_plan(g, pass, *dev);
+    *schedule = p.ok ? 1 : 0;
+    *cluster = p.ok ? p.K : 0;
+    return IABN_OK;
+}
+
+iabn_status iabn_forward(const iabn_desc* desc, const void* x, void* z, const float* gamma,
+                         const float* beta, float* running_mean, float* running_var,
+                         float* save_mean, float* save_var, float momentum, float eps,
+                         float slope, uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
+                          momentum, eps, slope, flags, c.g.m));
+    IABN_TRY(attach_device(c));
+    return DISPATCH(c.g.dtype, forward_impl, c, x, z, gamma, beta, running_mean, running_var,
+                    save_mean, save_var, momentum, eps, slope, flags);
+}
+
+iabn_status iabn_backward(const iabn_desc* desc, const void* z, const void* dz, void* dx,
+                          const float* gamma, const float* beta, const float* save_mean,
+                          const float* save_var, float* dgamma, float* dbeta, float eps,
+                          float slope, uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    (void)save_mean;  // BN* does not depend on mu_B
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
+    IABN_TRY(attach_device(c));
+    return DISPATCH(c.g.dtype, backward_impl, c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta,
+                    eps, slope, flags);
+}
+
+// ---------------------------------------------------------------- split phase
+iabn_status iabn_forward_reduce(const iabn_desc* desc, const void* x, double* stats, void* ws,
+                                size_t ws_bytes, void* stream) {
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    IABN_TRY(check_act("x", x));
+    if (!stats) return fail(IABN_ERR_INVALID_ARG, "stats is NULL");
+    IABN_TRY(attach_device(c));
+    IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
+    combine_kernel<3><<<cgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
+                                                      -1.0);
+    return check_launch("combine kernel");
+}
+
+iabn_status iabn_forward_apply(const iabn_desc* desc, const void* x, void* z,
+                               const double* stats_global, const float* gamma, const float* beta,
+                               float* running_mean, float* running_var, float* save_mean,
+                               float* save_var, float momentum, float eps, float slope,
+                               uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    if (!stats_global) return fail(IABN_ERR_INVALID_ARG, "stats_global is NULL");
+    // the global count is on the device; only the local one can be checked here
+    IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
+                          momentum, eps, slope, flags & ~(uint32_t)IABN_EVAL, 2));
+    IABN_TRY(attach_device(c));
+    return DISPATCH(c.g.dtype, fwd_from_partials, c, stats_global, 1, x, z, gamma, beta,
+                    running_mean, running_var, save_mean, save_var, momentum, eps, slope, flags);
+}
+
+iabn_status iabn_backward_reduce(const iabn_desc* desc, const void* z, const void* dz,
+                                 const float* gamma, const float* beta, double* sums, float eps,
+                                 float slope, uint32_t flags, void* ws, size_t ws_bytes,
+                                 void* stream) {
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    IABN_TRY(check_act("z", z));
+    IABN_TRY(check_act("dz", dz));
+    if (!gamma || !beta || !sums) return fail(IABN_ERR_INVALID_ARG, "gamma/beta/sums is NULL");
+    IABN_TRY(check_scalars(eps, slope));
+    IABN_TRY(attach_device(c));
+    double* part = wsp<double>(c, c.w.part);
+    IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
+                      flags, part, c.st));
+    combine_kernel<2><<<cgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, sums, (double)c.g.m);
+    return check_launch("combine kernel");
+}
+
+iabn_status iabn_backward_apply(const iabn_desc* desc, const void* z, const void* dz, void* dx,
+                                const double* sums_global, const double* sums_local,
+                                const float* gamma, const float* beta, const float* save_var,
+                                float* dgamma, float* dbeta, float eps, float slope,
+                                uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
+    if (!sums_global) return fail(IABN_ERR_INVALID_ARG, "sums_global is NULL");
+    IABN_TRY(attach_device(c));
+    const double* loc = (flags & IABN_SYNC_GLOBAL_PARAM_GRADS) || !sums_local ? sums_global
+                                                                               : sums_local;
+    return DISPATCH(c.g.dtype, bwd_from_sums, c, sums_global, 1, loc, 1, sums_global + 2 * c.g.C,
+                    0.0, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope, flags);
+}
+
+// ---------------------------------------------------------------- synchronized
+iabn_status iabn_comm_get_unique_id(unsigned char id[128]) {
+    if (!id) return fail(IABN_ERR_INVALID_ARG, "id is NULL");
+    Nccl* n = nccl();
+    if (!n) return fail(IABN_ERR_NCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+    ncclUniqueId u;
+    const ncclResult_t r = n->GetUniqueId(&u);
+    if (r != ncclSuccess) return fail(IABN_ERR_NCCL, "ncclGetUniqueId: %s", n->GetErrorString(r));
+    static_assert(sizeof(u.internal) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(id, u.internal, 128);
+    return IABN_OK;
+}
+
+iabn_status iabn_comm_init(iabn_comm* out, int nranks, int rank, const unsigned char id[128]) {
+    if (!out || !id) return fail(IABN_ERR_INVALID_ARG, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(IABN_ERR_INVALID_ARG, "bad rank %d of %d", rank, nranks);
+    Nccl* n = nccl();
+    if (!n) return fail(IABN_ERR_NCCL, "NCCL unavailable: %s", g_nccl.why.c_str());
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    ncclComm_t comm;
+    const ncclResult_t r = n->CommInitRank(&comm, nranks, u, rank);
+    if (r != ncclSuccess) return fail(IABN_ERR_NCCL, "ncclCommInitRank: %s", n->GetErrorString(r));
+    *out = new iabn_comm_s{comm, nranks, rank};
+    return IABN_OK;
+}
+
+iabn_status iabn_comm_destroy(iabn_comm comm) {
+    if (!comm) return IABN_OK;
+    Nccl* n = nccl();
+    iabn_status s = IABN_OK;
+    if (n) {
+        const ncclResult_t r = n->CommDestroy(comm->comm);
+        if (r != ncclSuccess) s = fail(IABN_ERR_NCCL, "ncclCommDestroy: %s", n->GetErrorString(r));
+    }
+    delete comm;
+    return s;
+}
+
+iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, const float* gamma,
+                              const float* beta, float* running_mean, float* running_var,
+                              float* save_mean, float* save_var, float momentum, float eps,
+                              float slope, uint32_t flags, void* ws, size_t ws_bytes,
+                              void* stream, iabn_comm comm) {
+    if (!comm) return fail(IABN_ERR_INVALID_ARG, "comm is NULL");
+    if (comm->nranks == 1 || (flags & IABN_EVAL))
+        return iabn_forward(desc, x, z, gamma, beta, running_mean, running_var, save_mean,
+                            save_var, momentum, eps, slope, flags, ws, ws_bytes, stream);
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    // global count >= nranks * 1 >= 2
+    IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
+                          momentum, eps, slope, flags, c.g.m * comm->nranks));
+    IABN_TRY(attach_device(c));
+    double* stats = wsp<double>(c, c.w.stats);
+    IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
+    combine_kernel<3><<<cgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
+                                                      -1.0);
+    IABN_TRY(check_launch("combine kernel"));
+    IABN_TRY(allreduce_f64(stats, (size_t)c.g.C * 3, comm, c.st));
+    return DISPATCH(c.g.dtype, fwd_from_partials, c, stats, 1, x, z, gamma, beta, running_mean,
+                    running_var, save_mean, save_var, momentum, eps, slope, flags);
+}
+
+iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void* dz, void* dx,
+                               const float* gamma, const float* beta, const float* save_mean,
+                               const float* save_var, float* dgamma, float* dbeta, float eps,
+                               float slope, uint32_t flags, void* ws, size_t ws_bytes,
+                               void* stream, iabn_comm comm) {
+    if (!comm) return fail(IABN_ERR_INVALID_ARG, "comm is NULL");
+    if (comm->nranks == 1)
+        return iabn_backward(desc, z, dz, dx, gamma, beta, save_mean, save_var, dgamma, dbeta,
+                             eps, slope, flags, ws, ws_bytes, stream);
+    Ctx c;
+    IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
+    IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
+    IABN_TRY(attach_device(c));
+    double* part = wsp<double>(c, c.w.part);
+    double* loc = wsp<double>(c, c.w.sums_loc);
+    double* glob = wsp<double>(c, c.w.sums_glob);
+    IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
+                      flags, part, c.st));
+    combine_kernel<2><<<cgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, loc, (double)c.g.m);
+    IABN_TRY(check_launch("combine kernel"));
+    const size_t nb = (size_t)(2 * c.g.C + 1) * sizeof(double);
+    const cudaError_t e = cudaMemcpyAsync(glob, loc, nb, cudaMemcpyDeviceToDevice, c.st);
+    if (e != cudaSuccess) return fail(IABN_ERR_CUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
+    IABN_TRY(allreduce_f64(glob, (size_t)(2 * c.g.C + 1), comm, c.st));
+    const double* lsrc = (flags & IABN_SYNC_GLOBAL_PARAM_GRADS) ? glob : loc;
+    return DISPATCH(c.g.dtype, bwd_from_sums, c, glob, 1, lsrc, 1, glob + 2 * c.g.C, 0.0, z, dz,
+                    dx, gamma, beta, save_var, dgamma, dbeta, eps, slope, flags);
+}
+
+}  // extern "C"

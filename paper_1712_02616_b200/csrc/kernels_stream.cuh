@@ -1,0 +1,646 @@
+// kernels_stream.cuh -- streaming schedule of the InPlace-ABN hot path.
+//
+// Any layout / dtype / alignment.  Data are re-read after each global
+// dependency (per-channel statistics before normalising, gradient sums before
+// dx), so a pass over E elements of b bytes moves:
+//   forward : stats (read E*b) + apply (read E*b, write E*b)           = 3*E*b
+//   backward: reduce (read 2*E*b) + apply (read 2*E*b, write E*b)      = 5*E*b
+// The channel-resident schedule (kernels_fused.cuh) does 2*E*b and 3*E*b.
+//
+// Numerics (R8): per-thread fp32 partial sums in several independent
+// chains, shifted by a per-channel sample K (cancellation-free variance), flushed
+// into fp64 every few vectors; fp64 block/cross-block/cross-GPU combines as raw
+// moments (count, sum, sum of squares) -- deterministic trees, no atomics.
+#pragma once
+
+#include "common.cuh"
+
+namespace iabn {
+
+constexpr int kUnroll = 4;
+
+// Gamma reparametrisation (R4).
+enum : uint32_t { kGammaPlain = 1u << 0, kGammaFixedOne = 1u << 1, kRunVarBiased = 1u << 2 };
+
+__device__ __forceinline__ double gamma_eff(float gamma, float eps, uint32_t flags) {
+    if (flags & kGammaFixedOne) return 1.0;
+    if (flags & kGammaPlain) return (double)gamma;
+    return fabs((double)gamma) + (double)eps;
+}
+__device__ __forceinline__ double gamma_sign(float gamma, uint32_t flags) {
+    if (flags & (kGammaFixedOne | kGammaPlain)) return 1.0;
+    return gamma < 0.f ? -1.0 : 1.0;
+}
+
+// ====================================================================== F1: statistics
+// Raw fp64 moments of a block's values v_i, accumulated as shifted sums about K:
+//   count = n, sum = n K + S1, sumsq = S2 + 2 K S1 + n K^2,  S1 = sum (v-K), S2 = sum (v-K)^2
+__device__ __forceinline__ void write_raw_moments(double* out, double n, double K, double S1,
+                                                  double S2) {
+    out[0] = n;
+    out[1] = n * K + S1;
+    out[2] = S2 + 2.0 * K * S1 + n * K * K;
+}
+
+// NCHW: grid (C, S); CTA (c, s) reduces channel-space [lo, hi) of m = N*HW values;
+// channel-space index j lives at x[((j / HW) * C + c) * HW + j % HW].
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    stats_nchw_kernel(const T* __restrict__ x, int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw,
+                      double* __restrict__ part) {
+    constexpr int V = VEC ? Elem<T>::kVec : 1;
+    __shared__ double red[2 * kThreads / 32];
+    const int64_t c = blockIdx.x;
+    const int S = gridDim.y, s = blockIdx.y;
+    const uint32_t mv = m / V;
+    const uint32_t vlo = (uint32_t)((uint64_t)mv * s / S), vhi = (uint32_t)((uint64_t)mv * (s + 1) / S);
+    const float K = ld_scalar<T>(x + c * HW);
+    const T* xc = x + c * HW;
+    float a1[V], a2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
+    double d1 = 0.0, d2 = 0.0;
+    int iter = 0;
+    for (uint32_t base = vlo + threadIdx.x; base < vhi; base += kThreads * kUnroll) {
+        float f[kUnroll][V];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t v = base + u * kThreads;
+            if (v < vhi) {
+                const uint32_t j = v * V;
+                const uint32_t n = fdiv(j, fd_hw);
+                const T* p = xc + ((int64_t)n * C) * HW + (j - n * (uint32_t)HW);
+                if constexpr (VEC) {
+                    unpack<T>(ld_vec(p), f[u]);
+                } else {
+                    f[u][0] = ld_scalar<T>(p);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < V; ++k) f[u][k] = K;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const float dv = f[u][k] - K;
+                a1[k] += dv;
+                a2[k] = fmaf(dv, dv, a2[k]);
+            }
+        if (++iter == 16) {
+            iter = 0;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                d1 += a1[k];
+                d2 += a2[k];
+                a1[k] = a2[k] = 0.f;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        d1 += a1[k];
+        d2 += a2[k];
+    }
+    double v2[2] = {d1, d2};
+    block_sum<2>(v2, red);
+    if (threadIdx.x == 0)
+        write_raw_moments(part + ((int64_t)s * C + c) * 3, (double)(vhi - vlo) * V, K, v2[0],
+                          v2[1]);
+}
+
+// NHWC ([rows][C], rows = N*HW): block = 16 (channel groups of V) x 16 (rows);
+// grid (ceil(C / (16 V)), S); CTA reduces rows [rlo, rhi) for 16*V channels.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    stats_nhwc_kernel(const T* __restrict__ x, int64_t C, int64_t rows, double* __restrict__ part) {
+    constexpr int V = VEC ? Elem<T>::kVec : 1;
+    constexpr int CT = 16 * V;
+    __shared__ double red[16][CT][2];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int S = gridDim.y, s = blockIdx.y;
+    const int64_t c0 = (int64_t)blockIdx.x * CT + tx * V;
+    const int64_t rlo = rows * s / S, rhi = rows * (s + 1) / S;
+    const bool active = c0 < C;
+    float K[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) K[k] = (active && c0 + k < C) ? ld_scalar<T>(x + c0 + k) : 0.f;
+    float a1[V], a2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
+    double d1[V], d2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) d1[k] = d2[k] = 0.0;
+    if (active) {
+        int iter = 0;
+        for (int64_t r0 = rlo + ty; r0 < rhi; r0 += 16 * kUnroll) {
+            float f[kUnroll][V];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int64_t r = r0 + 16 * u;
+                if (r < rhi) {
+                    const T* p = x + r * C + c0;
+                    if constexpr (VEC) {
+                        unpack<T>(ld_vec(p), f[u]);
+                    } else {
+                        f[u][0] = ld_scalar<T>(p);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) f[u][k] = K[k];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    const float dv = f[u][k] - K[k];
+                    a1[k] += dv;
+                    a2[k] = fmaf(dv, dv, a2[k]);
+                }
+            if (++iter == 16) {
+                iter = 0;
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    d1[k] += a1[k];
+                    d2[k] += a2[k];
+                    a1[k] = a2[k] = 0.f;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        red[ty][tx * V + k][0] = d1[k] + a1[k];
+        red[ty][tx * V + k][1] = d2[k] + a2[k];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < CT) {
+        const int64_t c = (int64_t)blockIdx.x * CT + t;
+        if (c < C) {
+            double S1 = 0.0, S2 = 0.0;
+            for (int y = 0; y < 16; ++y) {
+                S1 += red[y][t][0];
+                S2 += red[y][t][1];
+            }
+            const double Kc = (double)ld_scalar<T>(x + c);
+            write_raw_moments(part + ((int64_t)s * C + c) * 3, (double)(rhi - rlo), Kc, S1, S2);
+        }
+    }
+}
+
+// Sum S partial records of NV doubles per channel in fixed order: out[c][k].
+// extra >= 0: out[NV*C] = extra (the count slot of the backward sums).
+template <int NV>
+__global__ void combine_kernel(const double* __restrict__ part, int S, int64_t C,
+                               double* __restrict__ out, double extra) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < C) {
+        double acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int k = 0; k < NV; ++k) acc[k] += part[((int64_t)s * C + c) * NV + k];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) out[c * NV + k] = acc[k];
+    }
+    if (c == 0 && extra >= 0.0) out[NV * C] = extra;
+}
+
+// F1 finalize (+F1' running stats): from S partial raw moments per channel to
+//   mean, biased var and the apply coefficients (A, mu_hi, mu_lo, beta) with
+//   A = g rstd, so that y = ((x - mu_hi) - mu_lo) A + beta.  The mean is carried
+//   as an fp32 pair: x - mu_hi is exact near the mean (Sterbenz), which keeps
+//   x^ accurate when |mean| >> std (R8).
+struct FwdCoefArgs {
+    const double* part;
+    int S;
+    int64_t C;
+    const float* gamma;
+    const float* beta;
+    float* running_mean;
+    float* running_var;
+    float* save_mean;
+    float* save_var;
+    float4* coef;
+    float momentum, eps;
+    uint32_t flags;
+};
+
+__device__ __forceinline__ float4 fwd_coef_from_moments(double cnt, double sum, double sumsq,
+                                                        float gamma, float beta, float eps,
+                                                        uint32_t flags, double* mean_out,
+                                                        double* var_out) {
+    const double mean = sum / cnt;
+    double var = sumsq / cnt - mean * mean;
+    var = var > 0.0 ? var : 0.0;
+    const double rstd = 1.0 / sqrt(var + (double)eps);
+    const double A = gamma_eff(gamma, eps, flags) * rstd;
+    const float mu_hi = (float)mean;
+    *mean_out = mean;
+    *var_out = var;
+    return make_float4((float)A, mu_hi, (float)(mean - (double)mu_hi), beta);
+}
+
+// y = ((x - mu_hi) - mu_lo) A + beta
+__device__ __forceinline__ float affine(float x, const float4& cf) {
+    return fmaf((x - cf.y) - cf.z, cf.x, cf.w);
+}
+
+__device__ __forceinline__ void update_running(float* rm, float* rv, int64_t c, double mean,
+                                               double var, double cnt, float momentum,
+                                               uint32_t flags) {
+    if (rm) rm[c] = (float)((1.0 - momentum) * (double)rm[c] + (double)momentum * mean);
+    if (rv) {
+        const double v = (flags & kRunVarBiased) ? var : var * cnt / (cnt - 1.0);
+        rv[c] = (float)((1.0 - momentum) * (double)rv[c] + (double)momentum * v);
+    }
+}
+
+__global__ void fwd_coef_kernel(FwdCoefArgs a) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.C) return;
+    double cnt = 0.0, sum = 0.0, sumsq = 0.0;
+    for (int s = 0; s < a.S; ++s) {
+        const double* p = a.part + ((int64_t)s * a.C + c) * 3;
+        cnt += p[0];
+        sum += p[1];
+        sumsq += p[2];
+    }
+    double mean, var;
+    a.coef[c] = fwd_coef_from_moments(cnt, sum, sumsq, a.gamma[c], a.beta[c], a.eps, a.flags,
+                                      &mean, &var);
+    if (a.save_mean) a.save_mean[c] = (float)mean;
+    if (a.save_var) a.save_var[c] = (float)var;
+    update_running(a.running_mean, a.running_var, c, mean, var, cnt, a.momentum, a.flags);
+}
+
+// Eval mode: fixed running statistics.
+__global__ void eval_coef_kernel(int64_t C, const float* __restrict__ gamma,
+                                 const float* __restrict__ beta, const float* __restrict__ rm,
+                                 const float* __restrict__ rv, float eps, uint32_t flags,
+                                 float4* __restrict__ coef) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    const double A = gamma_eff(gamma[c], eps, flags) / sqrt((double)rv[c] + (double)eps);
+    coef[c] = make_float4((float)A, rm[c], 0.f, beta[c]);
+}
+
+// ====================================================================== elementwise passes
+// Channel of flat element e (e < 2^32 within one launch; the host splits the
+// tensor into whole-sample chunks).
+template <int LAYOUT>
+__device__ __forceinline__ uint32_t channel_of(uint32_t e, const FastDiv& fd_hw,
+                                               const FastDiv& fd_c) {
+    if (LAYOUT == 0) {  // NCHW
+        const uint32_t p = fdiv(e, fd_hw);
+        return p - fdiv(p, fd_c) * fd_c.d;
+    }
+    return e - fdiv(e, fd_c) * fd_c.d;  // NHWC
+}
+
+__device__ __forceinline__ float leaky(float y, float slope) { return y >= 0.f ? y : y * slope; }
+
+// F2: z = f(x A_c + B_c), in place allowed (each element read then written by
+// the same thread).  ALIGNED: a 16-byte vector never spans two channels.
+template <typename T, int LAYOUT, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads)
+    fwd_apply_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
+                     FastDiv fd_c, float slope) {
+    constexpr int V = Elem<T>::kVec;
+    const uint32_t nvec = E / V;
+    const uint32_t stride = gridDim.x * kThreads;
+    for (uint32_t base = blockIdx.x * kThreads + threadIdx.x; base < nvec;
+         base += stride * kUnroll) {
+        uint4 r[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t v = base + u * stride;
+            if (v < nvec) r[u] = ld_vec(x + (size_t)v * V);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t v = base + u * stride;
+            if (v < nvec) {
+                float f[V];
+                unpack<T>(r[u], f);
+                const uint32_t e = v * V;
+                if (ALIGNED) {
+                    const float4 cf = __ldg(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
+#pragma unroll
+                    for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], cf), slope);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) {
+                        const float4 cf = __ldg(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
+                        f[k] = leaky(affine(f[k], cf), slope);
+                    }
+                }
+                st_vec(z + (size_t)v * V, pack<T>(f));
+            }
+        }
+    }
+    // tail (E % V elements) by the first threads of block 0
+    if (blockIdx.x == 0 && threadIdx.x < E - nvec * V) {
+        const uint32_t e = nvec * V + threadIdx.x;
+        const float4 cf = coef[channel_of<LAYOUT>(e, fd_hw, fd_c)];
+        st_scalar<T>(z + e, leaky(affine(ld_scalar<T>(x + e), cf), slope));
+    }
+}
+
+// ====================================================================== B1: gradient sums
+// Per element (Alg. 2 l.2-5): dy = f'(z) dz, y = f^-1(z),
+// x^ = (y - beta)/g = y * inv_g + nb;  per channel S1 = sum dy, S2 = sum dy x^.
+struct InvAffine {
+    float inv_g, nb;
+};
+__device__ __forceinline__ InvAffine inv_affine(float gamma, float beta, float eps, uint32_t flags) {
+    const double g = gamma_eff(gamma, eps, flags);
+    return {(float)(1.0 / g), (float)(-(double)beta / g)};
+}
+
+__device__ __forceinline__ void grad_terms(float z, float dz, float slope, float inv_slope,
+                                           InvAffine ia, float& dy, float& xh) {
+    const bool pos = z >= 0.f;  // sign(z) = sign(y) for slope > 0; -0.0 counts as >= 0
+    const float y = pos ? z : z * inv_slope;
+    dy = pos ? dz : dz * slope;
+    xh = fmaf(y, ia.inv_g, ia.nb);
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    bwd_reduce_nchw_kernel(const T* __restrict__ z, const T* __restrict__ dz,
+                           const float* __restrict__ gamma, const float* __restrict__ beta,
+                           int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw, float eps,
+                           float slope, float inv_slope, uint32_t flags,
+                           double* __restrict__ part) {
+    constexpr int V = VEC ? Elem<T>::kVec : 1;
+    __shared__ double red[2 * kThreads / 32];
+    const int64_t c = blockIdx.x;
+    const int S = gridDim.y, s = blockIdx.y;
+    const uint32_t mv = m / V;
+    const uint32_t vlo = (uint32_t)((uint64_t)mv * s / S), vhi = (uint32_t)((uint64_t)mv * (s + 1) / S);
+    const InvAffine ia = inv_affine(gamma[c], beta[c], eps, flags);
+    const T* zc = z + c * HW;
+    const T* dzc = dz + c * HW;
+    float a1[V], a2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
+    double d1 = 0.0, d2 = 0.0;
+    int iter = 0;
+    for (uint32_t base = vlo + threadIdx.x; base < vhi; base += kThreads * kUnroll) {
+        float fz[kUnroll][V], fd[kUnroll][V];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t v = base + u * kThreads;
+            if (v < vhi) {
+                const uint32_t j = v * V;
+                const uint32_t n = fdiv(j, fd_hw);
+                const int64_t off = ((int64_t)n * C) * HW + (j - n * (uint32_t)HW);
+                if constexpr (VEC) {
+                    unpack<T>(ld_vec(zc + off), fz[u]);
+                    unpack<T>(ld_vec(dzc + off), fd[u]);
+                } else {
+                    fz[u][0] = ld_scalar<T>(zc + off);
+                    fd[u][0] = ld_scalar<T>(dzc + off);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < V; ++k) fz[u][k] = fd[u][k] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                float dy, xh;
+                grad_terms(fz[u][k], fd[u][k], slope, inv_slope, ia, dy, xh);
+                a1[k] += dy;
+                a2[k] = fmaf(dy, xh, a2[k]);
+            }
+        if (++iter == 16) {
+            iter = 0;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                d1 += a1[k];
+                d2 += a2[k];
+                a1[k] = a2[k] = 0.f;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        d1 += a1[k];
+        d2 += a2[k];
+    }
+    double v2[2] = {d1, d2};
+    block_sum<2>(v2, red);
+    if (threadIdx.x == 0) {
+        double* o = part + ((int64_t)s * C + c) * 2;
+        o[0] = v2[0];
+        o[1] = v2[1];
+    }
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    bwd_reduce_nhwc_kernel(const T* __restrict__ z, const T* __restrict__ dz,
+                           const float* __restrict__ gamma, const float* __restrict__ beta,
+                           int64_t C, int64_t rows, float eps, float slope, float inv_slope,
+                           uint32_t flags, double* __restrict__ part) {
+    constexpr int V = VEC ? Elem<T>::kVec : 1;
+    constexpr int CT = 16 * V;
+    __shared__ double red[16][CT][2];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int S = gridDim.y, s = blockIdx.y;
+    const int64_t c0 = (int64_t)blockIdx.x * CT + tx * V;
+    const int64_t rlo = rows * s / S, rhi = rows * (s + 1) / S;
+    const bool active = c0 < C;
+    InvAffine ia[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+        ia[k] = (active && c0 + k < C) ? inv_affine(gamma[c0 + k], beta[c0 + k], eps, flags)
+                                       : InvAffine{0.f, 0.f};
+    float a1[V], a2[V];
+    double d1[V], d2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        a1[k] = a2[k] = 0.f;
+        d1[k] = d2[k] = 0.0;
+    }
+    if (active) {
+        int iter = 0;
+        for (int64_t r0 = rlo + ty; r0 < rhi; r0 += 16 * kUnroll) {
+            float fz[kUnroll][V], fd[kUnroll][V];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int64_t r = r0 + 16 * u;
+                if (r < rhi) {
+                    const int64_t off = r * C + c0;
+                    if constexpr (VEC) {
+                        unpack<T>(ld_vec(z + off), fz[u]);
+                        unpack<T>(ld_vec(dz + off), fd[u]);
+                    } else {
+                        fz[u][0] = ld_scalar<T>(z + off);
+                        fd[u][0] = ld_scalar<T>(dz + off);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) fz[u][k] = fd[u][k] = 0.f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    float dy, xh;
+                    grad_terms(fz[u][k], fd[u][k], slope, inv_slope, ia[k], dy, xh);
+                    a1[k] += dy;
+                    a2[k] = fmaf(dy, xh, a2[k]);
+                }
+            if (++iter == 16) {
+                iter = 0;
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    d1[k] += a1[k];
+                    d2[k] += a2[k];
+                    a1[k] = a2[k] = 0.f;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        red[ty][tx * V + k][0] = d1[k] + a1[k];
+        red[ty][tx * V + k][1] = d2[k] + a2[k];
+    }
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < CT) {
+        const int64_t c = (int64_t)blockIdx.x * CT + t;
+        if (c < C) {
+            double S1 = 0.0, S2 = 0.0;
+            for (int y = 0; y < 16; ++y) {
+                S1 += red[y][t][0];
+                S2 += red[y][t][1];
+            }
+            double* o = part + ((int64_t)s * C + c) * 2;
+            o[0] = S1;
+            o[1] = S2;
+        }
+    }
+}
+
+// B2 coefficients (refolded in y):
+//   dx = g rstd (dy - x^ S2/m - S1/m),  x^ = (y - beta)/g
+//      = alpha dy + kappa y + cc,  alpha = g rstd, kappa = -rstd S2/m,
+//        cc = rstd (S2/m) beta - g rstd S1/m
+// S1, S2, m: global (all ranks) sums; dgamma/dbeta from the local or global sums.
+struct BwdCoefArgs {
+    const double* glob;  // [S_glob][C][2]
+    int S_glob;
+    const double* loc;  // [S_loc][C][2]
+    int S_loc;
+    const double* count_ptr;  // device count (sync) or nullptr
+    double count;             // used when count_ptr == nullptr
+    int64_t C;
+    const float* gamma;
+    const float* beta;
+    const float* save_var;
+    float* dgamma;
+    float* dbeta;
+    float4* coef;
+    float eps;
+    uint32_t flags;
+};
+
+__device__ __forceinline__ float4 bwd_coef_from_sums(double S1, double S2, double m, float gamma,
+                                                     float beta, float var, float eps,
+                                                     uint32_t flags) {
+    const double g = gamma_eff(gamma, eps, flags);
+    const double rstd = 1.0 / sqrt((double)var + (double)eps);
+    const double alpha = g * rstd;
+    const double kappa = -rstd * S2 / m;
+    const double cc = rstd * (S2 / m) * (double)beta - g * rstd * S1 / m;
+    return make_float4((float)alpha, (float)kappa, (float)cc, 0.f);
+}
+
+__global__ void bwd_coef_kernel(BwdCoefArgs a) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.C) return;
+    double g1 = 0.0, g2 = 0.0, l1 = 0.0, l2 = 0.0;
+    for (int s = 0; s < a.S_glob; ++s) {
+        g1 += a.glob[((int64_t)s * a.C + c) * 2];
+        g2 += a.glob[((int64_t)s * a.C + c) * 2 + 1];
+    }
+    if (a.loc == a.glob) {
+        l1 = g1;
+        l2 = g2;
+    } else {
+        for (int s = 0; s < a.S_loc; ++s) {
+            l1 += a.loc[((int64_t)s * a.C + c) * 2];
+            l2 += a.loc[((int64_t)s * a.C + c) * 2 + 1];
+        }
+    }
+    const double m = a.count_ptr ? *a.count_ptr : a.count;
+    a.coef[c] = bwd_coef_from_sums(g1, g2, m, a.gamma[c], a.beta[c], a.save_var[c], a.eps, a.flags);
+    a.dbeta[c] = (float)l1;
+    a.dgamma[c] = (float)(gamma_sign(a.gamma[c], a.flags) * l2);
+}
+
+// B2: dx = alpha dy + kappa y + cc, dx may alias dz.
+template <typename T, int LAYOUT, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads)
+    bwd_apply_kernel(const T* __restrict__ z, const T* dz, T* dx, const float4* __restrict__ coef,
+                     uint32_t E, FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope) {
+    constexpr int V = Elem<T>::kVec;
+    const uint32_t nvec = E / V;
+    const uint32_t stride = gridDim.x * kThreads;
+    for (uint32_t base = blockIdx.x * kThreads + threadIdx.x; base < nvec;
+         base += stride * kUnroll) {
+        uint4 rz[kUnroll], rd[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t v = base + u * stride;
+            if (v < nvec) {
+                rz[u] = ld_vec(z + (size_t)v * V);
+                rd[u] = ld_vec(dz + (size_t)v * V);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const uint32_t v = base + u * stride;
+            if (v < nvec) {
+                float fz[V], fd[V];
+                unpack<T>(rz[u], fz);
+                unpack<T>(rd[u], fd);
+                const uint32_t e = v * V;
+                float4 cf;
+                if (ALIGNED) cf = __ldg(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    if (!ALIGNED) cf = __ldg(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
+                    const bool pos = fz[k] >= 0.f;
+                    const float y = pos ? fz[k] : fz[k] * inv_slope;
+                    const float dy = pos ? fd[k] : fd[k] * slope;
+                    fz[k] = fmaf(cf.x, dy, fmaf(cf.y, y, cf.z));
+                }
+                st_vec(dx + (size_t)v * V, pack<T>(fz));
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < E - nvec * V) {
+        const uint32_t e = nvec * V + threadIdx.x;
+        const float4 cf = coef[channel_of<LAYOUT>(e, fd_hw, fd_c)];
+        const float zz = ld_scalar<T>(z + e), dd = ld_scalar<T>(dz + e);
+        const bool pos = zz >= 0.f;
+        const float y = pos ? zz : zz * inv_slope;
+        const float dy = pos ? dd : dd * slope;
+        st_scalar<T>(dx + e, fmaf(cf.x, dy, fmaf(cf.y, y, cf.z)));
+    }
+}
+
+}  // namespace iabn

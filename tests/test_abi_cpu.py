@@ -1,0 +1,145 @@
+"""C-ABI library: loads without a GPU, exports every symbol include/iabn.h
+declares, and validates arguments synchronously before touching the device
+(so every error path below is exercised here, on CPU, with fake pointers that
+are never dereferenced)."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from paper_1712_02616_b200 import _lib as L
+
+# Calls that pass every host-side check would launch kernels on fake pointers
+# if a GPU were present; they only run where there is none.
+no_gpu = pytest.mark.skipif(torch.cuda.is_available(),
+                            reason="would launch kernels on fake pointers")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "iabn.h")
+
+P = 0x10000  # fake, 16-byte aligned "device" addresses (never dereferenced)
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"IABN_API\s+[\w\s\*]+?\b(iabn_\w+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol():
+    decl = declared_symbols()
+    assert len(decl) >= 17
+    assert sorted(decl) == sorted(L.EXPORTS)
+    for name in decl:
+        assert hasattr(L.lib, name), name
+
+
+def test_version_and_status_strings():
+    assert L.lib.iabn_version() == 1
+    names = [L.lib.iabn_status_string(s).decode() for s in range(8)]
+    assert names[0] == "IABN_OK" and names[3] == "IABN_ERR_ALIAS" and names[7] == "IABN_ERR_NCCL"
+
+
+def _fwd(d, x=P, z=P, gamma=P, beta=P, rm=P, rv=P, sm=P, sv=P, momentum=0.1, eps=1e-5,
+         slope=0.01, flags=0, ws=P * 16, ws_bytes=None):
+    if ws_bytes is None:
+        ws_bytes = L.workspace_bytes(d)
+    return L.lib.iabn_forward(ctypes.byref(d), x, z, gamma, beta, rm, rv, sm, sv, momentum, eps,
+                              slope, flags, ws, ws_bytes, None)
+
+
+def _bwd(d, z=P, dz=P * 4096, dx=P * 4096, gamma=P, beta=P, sv=P, dg=P, db=P, eps=1e-5,
+         slope=0.01, flags=0, ws=P * 16, ws_bytes=None):
+    if ws_bytes is None:
+        ws_bytes = L.workspace_bytes(d)
+    return L.lib.iabn_backward(ctypes.byref(d), z, dz, dx, gamma, beta, None, sv, dg, db, eps,
+                               slope, flags, ws, ws_bytes, None)
+
+
+def test_workspace_bytes():
+    assert L.workspace_bytes(L.desc(0, 4, 4, L.F32, L.NCHW)) == 0
+    assert L.workspace_bytes(L.desc(2, 8, 16, L.F32, L.NCHW)) > 0
+    a = L.workspace_bytes(L.desc(64, 1024, 196, L.F32, L.NCHW))
+    b = L.workspace_bytes(L.desc(16, 4096, 12544, L.BF16, L.NCHW))
+    assert a > 0 and b > 0 and b < 16 << 20  # O(C) scratch, never O(E)
+
+
+@pytest.mark.parametrize("n,c,hw", [(0, 4, 4), (2, 0, 4), (2, 4, 0), (-1, 4, 4)])
+def test_empty_shapes_rejected(n, c, hw):
+    d = L.desc(n, c, hw, L.F32, L.NCHW)
+    assert _fwd(d, ws_bytes=1 << 20) == L.ERR_INVALID_ARG
+    assert "empty" in L.lib.iabn_last_error().decode()
+
+
+def test_unknown_dtype_layout():
+    assert _fwd(L.desc(2, 4, 4, 7, L.NCHW), ws_bytes=1 << 20) == L.ERR_UNSUPPORTED
+    assert _fwd(L.desc(2, 4, 4, L.F32, 5), ws_bytes=1 << 20) == L.ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(eps=0.0), L.ERR_INVALID_ARG), (dict(eps=-1e-5), L.ERR_INVALID_ARG),
+    (dict(eps=float("inf")), L.ERR_INVALID_ARG), (dict(eps=float("nan")), L.ERR_INVALID_ARG),
+    (dict(slope=0.0), L.ERR_INVALID_ARG), (dict(slope=1.5), L.ERR_INVALID_ARG),
+    (dict(momentum=-0.1), L.ERR_INVALID_ARG), (dict(momentum=1.1), L.ERR_INVALID_ARG),
+    (dict(x=0), L.ERR_INVALID_ARG), (dict(gamma=0), L.ERR_INVALID_ARG),
+    (dict(sm=0), L.ERR_INVALID_ARG), (dict(rm=0), L.ERR_INVALID_ARG),
+    (dict(x=P + 4), L.ERR_UNSUPPORTED), (dict(z=P + 8), L.ERR_ALIAS),
+    (dict(ws=0), L.ERR_WORKSPACE), (dict(ws_bytes=16), L.ERR_WORKSPACE),
+])
+def test_forward_validation(kw, status):
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    if kw.get("z") == P + 8:  # 8 bytes past x: misaligned is checked first, so use +16
+        kw["z"] = P + 16
+    assert _fwd(d, **kw) == status, L.lib.iabn_last_error()
+
+
+def test_forward_degenerate_single_value():
+    d = L.desc(1, 8, 1, L.F32, L.NCHW)  # m = 1 value per channel
+    assert _fwd(d) == L.ERR_DEGENERATE
+
+
+@no_gpu
+def test_forward_momentum_zero_accepted_and_reaches_device():
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    # all host checks pass -> the call gets as far as the device (absent here)
+    st = _fwd(d, momentum=0.0, rm=0, rv=0)
+    assert st in (L.ERR_CUDA, L.OK)
+    if st == L.ERR_CUDA:
+        assert "cuda" in L.lib.iabn_last_error().decode().lower()
+
+
+@no_gpu
+def test_forward_in_place_allowed():
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    assert _fwd(d, x=P, z=P) in (L.ERR_CUDA, L.OK)
+    assert _fwd(d, x=P, z=P + 2 * 8 * 16 * 4) in (L.ERR_CUDA, L.OK)  # disjoint
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(dx=P * 4096 + 16), L.ERR_ALIAS),  # partial overlap of dx and dz
+    (dict(dx=P), L.ERR_ALIAS),  # dx overlaps z
+    (dict(sv=0), L.ERR_INVALID_ARG), (dict(dg=0), L.ERR_INVALID_ARG),
+    (dict(slope=2.0), L.ERR_INVALID_ARG), (dict(z=P + 2), L.ERR_UNSUPPORTED),
+])
+def test_backward_validation(kw, status):
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    assert _bwd(d, **kw) == status, L.lib.iabn_last_error()
+
+
+@no_gpu
+def test_backward_in_place_reaches_device():
+    d = L.desc(2, 8, 16, L.BF16, L.NHWC)
+    assert _bwd(d) in (L.ERR_CUDA, L.OK)
+
+
+@no_gpu
+def test_eval_needs_running_stats():
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    assert _fwd(d, rm=0, flags=L.EVAL) == L.ERR_INVALID_ARG
+    assert _fwd(d, sm=0, sv=0, flags=L.EVAL) in (L.ERR_CUDA, L.OK)
+
+
+@no_gpu
+def test_launch_count_is_zero_without_launches():
+    assert L.launch_count() == 0

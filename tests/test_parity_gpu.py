@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs, element by element (tests/harness.py for the metric,
+tolerances and the activation-branch reading R16)."""
+import numpy as np
+import pytest
+import torch
+
+import synth_inputs as S
+from tests.harness import Case, compare, inputs, run_gpu, run_oracle, to64
+from tests.util import chan_err, vec_err
+
+pytestmark = pytest.mark.gpu
+
+FUSED, STREAM = 1 << 9, 1 << 8
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1712_02616_b200  # noqa: F401  (fails loudly if libiabn.so is missing)
+
+
+def _check(case, flags=0, **kw):
+    x, dz, p = inputs(case)
+    got = run_gpu(case, x, dz, p, flags=flags, **kw)
+    ref = run_oracle(case, x, dz, p)
+    return compare(case, got, ref, p)
+
+
+# ------------------------------------------------------------------ cfg1 (BASELINE.json configs[0])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("flags", [0, STREAM], ids=["auto", "streaming"])
+def test_cfg1_tiny(seed, flags):
+    _check(Case(2, 8, 16, seed=seed), flags)
+
+
+def test_cfg1_tiny_is_fused_by_default():
+    from paper_1712_02616_b200 import _lib as L
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    assert L.query_schedule(d, 0) == (1, 1)
+    assert L.query_schedule(d, 1) == (1, 1)
+
+
+# ------------------------------------------------------------------ ragged / edge shapes
+EDGE = [
+    Case(3, 5, 7),                              # HW*4 not 16-aligned -> scalar streaming
+    Case(5, 37, 49, dtype="bf16"),              # 7x7 bf16
+    Case(4, 20, 196, dtype="bf16"),             # 14x14 bf16 (392 B planes, 8-aligned)
+    Case(4, 20, 196),                           # 14x14 fp32 (fused)
+    Case(1, 3, 2),                              # m = 2, the minimum for training
+    Case(2, 1, 4096),                           # one channel
+    Case(7, 64, 12, layout="NHWC"),             # NHWC, aligned channels
+    Case(3, 37, 10, layout="NHWC"),             # NHWC, C*4 not 16-aligned
+    Case(2, 136, 9, dtype="bf16", layout="NHWC"),
+    Case(9, 300, 64, dtype="bf16"),             # several CTAs per channel, ragged split
+    Case(33, 3, 1000),                          # many planes, few channels
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=lambda c: f"{c.N}x{c.C}x{c.HW}-{c.dtype}-{c.layout}")
+@pytest.mark.parametrize("flags", [0, STREAM], ids=["auto", "streaming"])
+def test_edge_shapes(case, flags):
+    _check(case, flags)
+
+
+@pytest.mark.parametrize("gamma_mode", ["plain", "fixed_one"])
+def test_gamma_modes(gamma_mode):
+    _check(Case(4, 24, 64, gamma_mode=gamma_mode, seed=3))
+    _check(Case(4, 24, 64, gamma_mode=gamma_mode, seed=3), STREAM)
+
+
+@pytest.mark.parametrize("slope", [0.01, 0.1, 1.0])
+def test_slopes(slope):
+    _check(Case(4, 16, 100, slope=slope, seed=4))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_stress_offset(dtype):
+    """|mean|/std = 1e3: cancellation in the variance (R8)."""
+    _check(Case(8, 16, 256, dtype=dtype, stress="offset", seed=5))
+    _check(Case(8, 16, 256, dtype=dtype, stress="offset", seed=5), STREAM)
+
+
+def test_stress_constant_channel():
+    _check(Case(8, 16, 256, stress="constant", seed=6))
+    _check(Case(8, 16, 256, stress="constant", seed=6), STREAM)
+
+
+def test_momentum_extremes():
+    _check(Case(4, 8, 32, momentum=0.0))
+    _check(Case(4, 8, 32, momentum=1.0))
+
+
+def test_out_of_place_bitwise_equal_to_in_place():
+    case = Case(6, 40, 196, seed=7)
+    x, dz, p = inputs(case)
+    for flags in (0, STREAM):
+        a = run_gpu(case, x, dz, p, flags=flags)
+        b = run_gpu(case, x, dz, p, flags=flags, inplace=False, dx_inplace=False)
+        for k in a:
+            assert torch.equal(a[k], b[k]), (flags, k)
+
+
+def test_deterministic():
+    case = Case(16, 64, 784, dtype="bf16", seed=8)
+    x, dz, p = inputs(case)
+    for flags in (0, STREAM):
+        a = run_gpu(case, x, dz, p, flags=flags)
+        b = run_gpu(case, x, dz, p, flags=flags)
+        for k in a:
+            assert torch.equal(a[k], b[k]), (flags, k)
+
+
+def test_fused_and_streaming_agree():
+    case = Case(8, 32, 784, seed=9)
+    x, dz, p = inputs(case)
+    a = run_gpu(case, x, dz, p, flags=FUSED)
+    b = run_gpu(case, x, dz, p, flags=STREAM)
+    for k in ("z", "dx"):
+        assert chan_err(to64(a[k]), to64(b[k]), 1) < 1e-5
+    for k in ("mean", "var", "dgamma", "dbeta"):
+        assert vec_err(to64(a[k]), to64(b[k])) < 1e-5
+
+
+def test_eval_mode():
+    import oracle
+    import paper_1712_02616_b200 as P
+    case = Case(4, 12, 50, seed=10)
+    x, _, p = inputs(case)
+    rm = torch.randn(12) * 0.1
+    rv = torch.rand(12) + 0.5
+    z, sm, sv = P.forward(x.cuda(), p.gamma.cuda(), p.beta.cuda(), rm.cuda(), rv.cuda(),
+                          training=False)
+    assert sm is None and sv is None
+    ref = oracle.load().forward_eval(to64(x), to64(p.gamma), to64(p.beta), to64(rm), to64(rv))
+    assert chan_err(to64(z), ref, 1) < 1e-5
+
+
+# ------------------------------------------------------------------ cfg2 (BASELINE.json configs[1]) full size
+@pytest.mark.parametrize("flags", [0, STREAM], ids=["fused", "streaming"])
+def test_cfg2_r50_stage3_full(flags):
+    errs = _check(Case(64, 1024, 196, seed=0), flags)
+    assert errs["z"] < 1e-5
+
+
+def test_cfg2_nhwc_full():
+    _check(Case(64, 1024, 196, layout="NHWC", seed=1))
+
+
+# ------------------------------------------------------------------ sync variant on one GPU (split phase)
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_sync_split_phase_equals_concatenated_batch(G, dtype):
+    """InPlace-ABN^sync: shards' statistics and gradient sums are
+    summed (torch.add here standing in for the NCCL all-reduce), and the result
+    must equal the oracle on the concatenated batch.  Shards have unequal N."""
+    import paper_1712_02616_b200 as P
+    case = Case(11, 24, 100, dtype=dtype, seed=11)
+    x, dz, p = inputs(case)
+    ref = run_oracle(case, x, dz, p)
+    bounds = np.linspace(0, case.N, G + 1).astype(int)
+    bounds[1] = max(bounds[1] - 1, 1)  # unequal shards
+    xs = [x[bounds[i]:bounds[i + 1]].cuda().contiguous() for i in range(G)]
+    dzs = [dz[bounds[i]:bounds[i + 1]].cuda().contiguous() for i in range(G)]
+    g, b = p.gamma.cuda(), p.beta.cuda()
+    stats = [P.forward_reduce(xi) for xi in xs]
+    tot = torch.stack(stats).sum(0)
+    zs, svs = [], []
+    for xi in xs:
+        rm, rv = p.running_mean.cuda(), p.running_var.cuda()
+        zi, smi, svi = P.forward_apply(xi, tot, g, b, rm, rv)
+        zs.append(zi)
+        svs.append(svi)
+    sums = [P.backward_reduce(zi, dzi, g, b) for zi, dzi in zip(zs, dzs)]
+    gsum = torch.stack(sums).sum(0)
+    dxs, dgs, dbs = [], [], []
+    for zi, dzi, si in zip(zs, dzs, sums):
+        dxi, dgi, dbi = P.backward_apply(zi, dzi, gsum, si, g, b, svs[0])
+        dxs.append(dxi)
+        dgs.append(dgi)
+        dbs.append(dbi)
+    torch.cuda.synchronize()
+    got = dict(z=torch.cat([t.cpu() for t in zs]), dx=torch.cat([t.cpu() for t in dxs]),
+               mean=smi.cpu(), var=svs[0].cpu(), rm=rm.cpu(), rv=rv.cpu(),
+               dgamma=sum(t.cpu() for t in dgs), dbeta=sum(t.cpu() for t in dbs))
+    compare(case, got, ref, p)
+    # every shard saw the same (global) statistics
+    for svi in svs[1:]:
+        assert torch.equal(svi, svs[0])
+    # global-param-grads flag returns the all-shard sums directly
+    _, dgg, dbg = P.backward_apply(zs[0], dzs[0].clone(), gsum, sums[0], g, b, svs[0],
+                                   dx=torch.empty_like(zs[0]), global_param_grads=True)
+    assert vec_err(to64(dgg), ref["dgamma"]) < 1e-4 * (50 if dtype == "bf16" else 1)
+    assert vec_err(to64(dbg), ref["dbeta"]) < 1e-4 * (50 if dtype == "bf16" else 1)
+
+
+# ------------------------------------------------------------------ autograd wrapper
+def test_autograd_module_matches_oracle():
+    import paper_1712_02616_b200 as P
+    import oracle
+    case = Case(4, 16, 64, seed=12)
+    x, dz, p = inputs(case)
+    m = P.InPlaceABN(16, device="cuda")
+    with torch.no_grad():
+        m.weight.copy_(p.gamma)
+        m.bias.copy_(p.beta)
+    xin = x.view(4, 16, 8, 8).cuda().requires_grad_(True)
+    h = xin * 1.0  # leaf can't be modified in place
+    z = m(h)
+    z.backward(dz.view(4, 16, 8, 8).cuda())
+    o = oracle.load()
+    f = o.forward(to64(x), to64(p.gamma), to64(p.beta))
+    dx, dg, db = o.backward_standard(to64(x), to64(dz), to64(p.gamma), to64(p.beta))
+    assert chan_err(to64(z.detach().view(4, 16, 64)), f.z, 1) < 1e-4
+    assert chan_err(to64(xin.grad.view(4, 16, 64)), dx, 1) < 1e-4
+    assert vec_err(to64(m.weight.grad), dg) < 1e-4 and vec_err(to64(m.bias.grad), db) < 1e-4
+
+
+def test_channels_last_module():
+    import paper_1712_02616_b200 as P
+    import oracle
+    case = Case(2, 32, 36, seed=13)
+    x, dz, p = inputs(case)
+    m = P.InPlaceABN(32, device="cuda")
+    with torch.no_grad():
+        m.weight.copy_(p.gamma)
+        m.bias.copy_(p.beta)
+    xin = x.view(2, 32, 6, 6).cuda().to(memory_format=torch.channels_last)
+    z = m(xin.clone())
+    ref = oracle.load().forward(to64(x), to64(p.gamma), to64(p.beta))
+    assert chan_err(to64(z.contiguous().view(2, 32, 36)), ref.z, 1) < 1e-4
+
+
+# ------------------------------------------------------------------ native code is what runs
+def test_kernels_launch_through_the_library():
+    from paper_1712_02616_b200 import _lib as L
+    before = L.launch_count()
+    _check(Case(2, 8, 16))
+    assert L.launch_count() - before >= 2
+    import os
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert "libiabn.so" in maps
