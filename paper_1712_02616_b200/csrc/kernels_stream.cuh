@@ -304,8 +304,11 @@ __device__ __forceinline__ uint32_t channel_of(uint32_t e, const FastDiv& fd_hw,
 
 __device__ __forceinline__ float leaky(float y, float slope) { return y >= 0.f ? y : y * slope; }
 
-// F2: z = f(x A_c + B_c), in place allowed (each element read then written by
-// the same thread).  ALIGNED: a 16-byte vector never spans two channels.
+// F2: z = f(y), y = ((x - mu_hi) - mu_lo) A + beta, in place allowed (each
+// element is read then written by the same thread).  ALIGNED: NCHW with HW*b a
+// multiple of 16 (a 16-byte vector lies in one channel) or NHWC with C*b a
+// multiple of 16 (a vector holds channels c0 .. c0+V-1); otherwise the channel
+// is resolved per element.
 template <typename T, int LAYOUT, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
@@ -328,10 +331,14 @@ __global__ void __launch_bounds__(kThreads)
                 float f[V];
                 unpack<T>(r[u], f);
                 const uint32_t e = v * V;
-                if (ALIGNED) {
+                if (ALIGNED && LAYOUT == 0) {  // NCHW: the vector lies in one channel
                     const float4 cf = __ldg(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
 #pragma unroll
                     for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], cf), slope);
+                } else if (ALIGNED) {  // NHWC, C % V == 0: channels c0 .. c0+V-1
+                    const uint32_t c0 = channel_of<LAYOUT>(e, fd_hw, fd_c);
+#pragma unroll
+                    for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], __ldg(coef + c0 + k)), slope);
                 } else {
 #pragma unroll
                     for (int k = 0; k < V; ++k) {
@@ -619,9 +626,12 @@ __global__ void __launch_bounds__(kThreads)
                 unpack<T>(rd[u], fd);
                 const uint32_t e = v * V;
                 float4 cf;
-                if (ALIGNED) cf = __ldg(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
+                uint32_t c0 = 0;
+                if (ALIGNED) c0 = channel_of<LAYOUT>(e, fd_hw, fd_c);
+                if (ALIGNED && LAYOUT == 0) cf = __ldg(coef + c0);  // NCHW: one channel
 #pragma unroll
                 for (int k = 0; k < V; ++k) {
+                    if (ALIGNED && LAYOUT == 1) cf = __ldg(coef + c0 + k);  // NHWC: c0 + k
                     if (!ALIGNED) cf = __ldg(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
                     const bool pos = fz[k] >= 0.f;
                     const float y = pos ? fz[k] : fz[k] * inv_slope;

@@ -48,7 +48,9 @@ EDGE = [
     Case(5, 37, 49, dtype="bf16"),              # 7x7 bf16
     Case(4, 20, 196, dtype="bf16"),             # 14x14 bf16 (392 B planes, 8-aligned)
     Case(4, 20, 196),                           # 14x14 fp32 (fused)
-    Case(1, 3, 2),                              # m = 2, the minimum for training
+    # m = 2, the minimum for training.  dx = g rstd (dy1-dy2) eps/(2(var+eps)): with
+    # eps << var it is a cancellation fp32 cannot resolve, so eps is taken large here.
+    Case(1, 3, 2, eps=0.5),
     Case(2, 1, 4096),                           # one channel
     Case(7, 64, 12, layout="NHWC"),             # NHWC, aligned channels
     Case(3, 37, 10, layout="NHWC"),             # NHWC, C*4 not 16-aligned
