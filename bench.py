@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--schedule", choices=["auto", "streaming", "fused"], default="auto",
+                    help="schedule override (IABN_FORCE_*), for experiments")
     return ap.parse_args()
 
 
@@ -291,9 +293,11 @@ def main():
 
     # keep the repeated in-place application bounded: re-standardise x and dz once
     # outside the timed region if they drift (z of a layer is the next layer's input)
+    fl = {"auto": 0, "streaming": L.FORCE_STREAMING, "fused": L.FORCE_FUSED}[args.schedule]
+
     def step():
-        z, sm, sv = P.forward(x, g, bt, rm, rv, comm=comm)
-        P.backward(z, dz, g, bt, sv, comm=comm)
+        z, sm, sv = P.forward(x, g, bt, rm, rv, comm=comm, flags=fl)
+        P.backward(z, dz, g, bt, sv, comm=comm, flags=fl)
 
     fits_l2 = 2 * E * b < 2 * L2_BYTES
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if fits_l2 else None
@@ -317,9 +321,9 @@ def main():
             if flush is not None:  # L2-resident workload: flush, time the step alone
                 flush.add_(1.0)
             evs[i][0].record(st)
-            z, sm, sv = P.forward(x, g, bt, rm, rv, comm=comm)
+            z, sm, sv = P.forward(x, g, bt, rm, rv, comm=comm, flags=fl)
             evs[i][1].record(st)
-            P.backward(z, dz, g, bt, sv, comm=comm)
+            P.backward(z, dz, g, bt, sv, comm=comm, flags=fl)
             evs[i][2].record(st)
         t_end.record(st)
         torch.cuda.synchronize()
@@ -357,9 +361,9 @@ def main():
     bwd_ms = bwd_sum / K
     fwd_ms = fwd_sum / K
     s_f, k_f = L.query_schedule(L.desc(N_local, C, HW, L.BF16 if b == 2 else L.F32, L.NCHW), 0,
-                                0 if world == 1 else L.FORCE_STREAMING)
+                                fl if world == 1 else L.FORCE_STREAMING)
     s_b, k_b = L.query_schedule(L.desc(N_local, C, HW, L.BF16 if b == 2 else L.F32, L.NCHW), 1,
-                                0 if world == 1 else L.FORCE_STREAMING)
+                                fl if world == 1 else L.FORCE_STREAMING)
     bwd_bytes = 3 * E * b
     achieved = bwd_bytes / (bwd_ms * 1e-3) / 1e9
     traffic = load_traffic(args.config) if world == 1 else None

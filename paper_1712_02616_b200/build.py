@@ -55,6 +55,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
            "-o", tmp, os.path.join(CSRC, "iabn.cu"), "-ldl"]
     if ptxas_v:
         cmd[1:1] = ["-Xptxas", "-v"]
+    extra = os.environ.get("IABN_NVCC_EXTRA", "").split()  # experiments (e.g. -DIABN_APPLY_WARPS=4)
+    cmd[1:1] = extra
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)

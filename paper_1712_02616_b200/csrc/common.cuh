@@ -166,13 +166,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    // try_wait suspends the warp in hardware until the phase completes (or the
+    // time hint expires), so waiting warps do not burn issue slots spinning.
     const uint32_t a = smem_addr(bar);
     asm volatile(
         "{\n\t.reg .pred P;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
         "@!P bra WAIT_%=;\n}" ::"r"(a),
-        "r"(parity)
+        "r"(parity), "n"(0x100000)
         : "memory");
 }
 // global -> shared bulk copy (TMA engine, SASS UBLKCP), completion counted on bar.
@@ -210,8 +212,95 @@ __device__ __forceinline__ double ld_dsmem_f64(const double* local_ptr, uint32_t
                  : "=r"(remote)
                  : "r"(smem_addr(local_ptr)), "r"(rank));
     double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote));
     return v;
 }
 
+}  // namespace iabn
+
+namespace iabn {
+// ------------------------------------------------------------------ packed fp32x2 math (sm_100a:
+// FADD2 / FMUL2 / FFMA2 -- two fp32 lanes per instruction)
+__device__ __forceinline__ unsigned long long f2_bits(float2 a) {
+    return ((unsigned long long)__float_as_uint(a.y) << 32) | __float_as_uint(a.x);
+}
+__device__ __forceinline__ float2 f2_from(unsigned long long b) {
+    return make_float2(__uint_as_float((uint32_t)b), __uint_as_float((uint32_t)(b >> 32)));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return f2_from(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return f2_from(d);
+}
+
+// bf16 pair (one 32-bit word) -> fp32 pair, exact.
+__device__ __forceinline__ float2 bf16x2_to_f2(uint32_t w) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+// (lo - k, hi - k) in fp32 straight from a bf16 pair: mixed-precision sub.f32.bf16
+// (SASS FHADD.BF16 with half select, no separate unpack).
+__device__ __forceinline__ float2 bf16x2_sub_f2(uint32_t w, float k) {
+    float a, b;
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+        "sub.f32.bf16 %0, lo, %3;\n\tsub.f32.bf16 %1, hi, %3;\n}"
+        : "=f"(a), "=f"(b)
+        : "r"(w), "f"(k));
+    return make_float2(a, b);
+}
+// fp32 pair -> bf16 pair, round to nearest even (F2FP.BF16.F32.PACK_AB).
+__device__ __forceinline__ uint32_t f2_to_bf16x2(float2 v) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// A 16-byte vector as fp32 pairs: 4 pairs (bf16) or 2 pairs (fp32).
+template <typename T>
+struct Pairs;
+template <>
+struct Pairs<float> {
+    static constexpr int kN = 2;
+    __device__ __forceinline__ static void load(const uint4& u, float2* p) {
+        p[0] = make_float2(__uint_as_float(u.x), __uint_as_float(u.y));
+        p[1] = make_float2(__uint_as_float(u.z), __uint_as_float(u.w));
+    }
+    __device__ __forceinline__ static void load_sub(const uint4& u, float k, float2* p) {
+        load(u, p);
+        p[0] = add2(p[0], make_float2(-k, -k));
+        p[1] = add2(p[1], make_float2(-k, -k));
+    }
+    __device__ __forceinline__ static uint4 store(const float2* p) {
+        return make_uint4(__float_as_uint(p[0].x), __float_as_uint(p[0].y), __float_as_uint(p[1].x),
+                          __float_as_uint(p[1].y));
+    }
+};
+template <>
+struct Pairs<__nv_bfloat16> {
+    static constexpr int kN = 4;
+    __device__ __forceinline__ static void load(const uint4& u, float2* p) {
+        p[0] = bf16x2_to_f2(u.x);
+        p[1] = bf16x2_to_f2(u.y);
+        p[2] = bf16x2_to_f2(u.z);
+        p[3] = bf16x2_to_f2(u.w);
+    }
+    __device__ __forceinline__ static void load_sub(const uint4& u, float k, float2* p) {
+        p[0] = bf16x2_sub_f2(u.x, k);
+        p[1] = bf16x2_sub_f2(u.y, k);
+        p[2] = bf16x2_sub_f2(u.z, k);
+        p[3] = bf16x2_sub_f2(u.w, k);
+    }
+    __device__ __forceinline__ static uint4 store(const float2* p) {
+        return make_uint4(f2_to_bf16x2(p[0]), f2_to_bf16x2(p[1]), f2_to_bf16x2(p[2]),
+                          f2_to_bf16x2(p[3]));
+    }
+};
 }  // namespace iabn

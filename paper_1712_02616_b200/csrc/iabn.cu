@@ -28,6 +28,9 @@ using namespace iabn;
 namespace {
 
 thread_local std::string g_err;
+unsigned long long* g_trace = nullptr;  // debug trace of the last fused launch
+size_t g_trace_n = 0;
+uint32_t g_trace_ch = 0;
 std::atomic<uint64_t> g_launches{0};
 
 iabn_status fail(iabn_status s, const char* fmt, ...) {
@@ -77,10 +80,10 @@ iabn_status device_facts(DevFacts** out) {
     }
     if (!f.attrs_set) {
         const int dyn = f.max_smem_optin - 4096;  // leave room for static smem
-        const void* fns[] = {(const void*)fused_fwd_kernel<float>,
-                             (const void*)fused_fwd_kernel<__nv_bfloat16>,
-                             (const void*)fused_bwd_kernel<float>,
-                             (const void*)fused_bwd_kernel<__nv_bfloat16>};
+        const void* fns[] = {(const void*)fused_kernel<float, 0>,
+                             (const void*)fused_kernel<__nv_bfloat16, 0>,
+                             (const void*)fused_kernel<float, 1>,
+                             (const void*)fused_kernel<__nv_bfloat16, 1>};
         for (const void* fn : fns) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -224,89 +227,174 @@ iabn_status check_ws(const Geom& g, void* ws, size_t ws_bytes, const WsLayout& w
 }
 
 // ====================================================================== fused planning
+int env_int(const char* name, int dflt) {
+    const char* s = getenv(name);
+    return s ? atoi(s) : dflt;
+}
+
+// Shared-memory budget per CTA for the slab ring: ~100 KB keeps two CTAs per SM.
 size_t fused_budget_bytes() {
-    static size_t budget = [] {
-        const char* s = getenv("IABN_FUSED_SMEM_KB");
-        const long kb = s ? atol(s) : 100;
-        return (size_t)(kb > 0 ? kb : 100) * 1024;
-    }();
+    static const size_t budget = (size_t)std::max(8, env_int("IABN_FUSED_SMEM_KB", 100)) * 1024;
     return budget;
 }
 
+
 struct FusedPlan {
     bool ok = false;
-    int K = 0;
+    int K = 0;           // CTAs per cluster (per channel)
+    int clusters = 0;    // persistent clusters in the grid
+    uint32_t cap = 0;    // vectors per input per buffer
     uint32_t chunk_vecs = 0;
+    int nbuf = 0;
     size_t smem = 0;
 };
 
-FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
-    FusedPlan p;
-    if (g.layout != IABN_NCHW || (g.HW * g.b) % 16 != 0) return p;
-    const int nin = pass == 0 ? 1 : 2;
-    const int64_t mv = g.m * g.b / 16;
-    const size_t budget = std::min<size_t>(fused_budget_bytes(), (size_t)f.max_smem_optin - 4096);
-    for (int K = 1; K <= 16 && K <= mv; ++K) {
-        const int64_t per = (mv + K - 1) / K;
-        const size_t bytes = (size_t)per * 16 * nin;
-        if (bytes <= budget) {
-            p.K = K;
-            p.smem = bytes;
-            const int64_t cv = std::max<int64_t>(512 / nin, (per + kMaxChunks - 1) / kMaxChunks);
-            p.chunk_vecs = (uint32_t)cv;
-            p.ok = true;
-            break;
-        }
-    }
-    if (!p.ok) return p;
-    // the cluster must be schedulable (K CTAs with this much shared memory)
+const void* fused_fn(int pass, int dtype) {
+    if (pass == 0)
+        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0>
+                                 : (const void*)fused_kernel<__nv_bfloat16, 0>;
+    return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1>
+                             : (const void*)fused_kernel<__nv_bfloat16, 1>;
+}
+
+// Co-resident clusters of K CTAs with `smem` bytes of dynamic shared memory (cached).
+int max_active_clusters(int pass, int dtype, int K, size_t smem) {
     static std::mutex mu;
-    static int cache_key[64][2][2][17];
-    static int cache_val[64][2][2][17];
+    struct Key {
+        int dev, pass, dtype, K;
+        size_t smem;
+        int val;
+    };
+    static Key cache[512];
+    static int ncache = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    const int di = dev & 63, ti = g.dtype;
     std::lock_guard<std::mutex> lk(mu);
-    int& key = cache_key[di][pass][ti][p.K];
-    int& val = cache_val[di][pass][ti][p.K];
-    const int want = (int)((p.smem + 1023) / 1024);
-    if (key < want || key == 0) {  // probe (monotone in smem)
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(p.K * 2), 1, 1);
-        cfg.blockDim = dim3(kThreads, 1, 1);
-        cfg.dynamicSmemBytes = p.smem;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = p.K;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int n = 0;
-        const void* fn = pass == 0 ? (g.dtype == IABN_F32 ? (const void*)fused_fwd_kernel<float>
-                                                          : (const void*)fused_fwd_kernel<__nv_bfloat16>)
-                                   : (g.dtype == IABN_F32 ? (const void*)fused_bwd_kernel<float>
-                                                          : (const void*)fused_bwd_kernel<__nv_bfloat16>);
-        const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, fn, &cfg);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            n = 0;
-        }
-        key = want;
-        val = n;
+    for (int i = 0; i < ncache; ++i)
+        if (cache[i].dev == dev && cache[i].pass == pass && cache[i].dtype == dtype &&
+            cache[i].K == K && cache[i].smem == smem)
+            return cache[i].val;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)K, 1, 1);
+    cfg.blockDim = dim3(kFusedThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fused_fn(pass, dtype), &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
     }
-    if (val <= 0) p.ok = false;
-    return p;
+    if (ncache < 512) cache[ncache++] = Key{dev, pass, dtype, K, smem, n};
+    return n;
+}
+
+// Choose (K, nbuf): a slice of ceil(mv/K) vectors per CTA, nbuf slab buffers.
+// Measured on B200 (profiles/): two ~100 KB CTAs per SM
+// beat one ~200 KB CTA (two independent pipelines hide each other's serial
+// phases), double buffering beats single when the slice allows it, and clusters
+// of <= 8 CTAs pack the GPCs far better than 16.  So: the smallest K whose slice
+// double-buffers in the per-CTA budget; else (large channels) the smallest K
+// whose slice fits once.
+FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
+    FusedPlan best;
+    if (g.layout != IABN_NCHW || (g.HW * g.b) % 16 != 0) return best;
+    const int nin = pass == 0 ? 1 : 2;
+    const int64_t mv = g.m * g.b / 16;
+    const size_t cap_bytes = (size_t)f.max_smem_optin - 4096;
+    const size_t budget = std::min<size_t>(fused_budget_bytes(), cap_bytes);
+    const int kforce = env_int("IABN_FUSED_K", 0);
+    const int nforce = env_int("IABN_FUSED_NBUF", 0);
+    const int64_t pv = g.HW * g.b / 16;  // vectors per plane
+    const int64_t np = g.N;
+    auto consider = [&](int K, int nbuf) -> bool {
+        // slice: whole planes when N >= K (see cta_slice)
+        const bool by_plane = np >= K;
+        const int64_t cap = by_plane ? pv * ((np + K - 1) / K) : (mv + K - 1) / K;
+        const size_t bytes = (size_t)cap * 16 * nin * nbuf;
+        if (bytes > budget) return false;
+        const int cl = max_active_clusters(pass, g.dtype, K, bytes);
+        if (cl <= 0) return false;
+        best.ok = true;
+        best.K = K;
+        best.clusters = (int)std::min<int64_t>(cl, g.C);
+        best.cap = (uint32_t)cap;
+        best.nbuf = nbuf;
+        best.smem = bytes;
+        // chunks: large bulk copies keep the TMA engines efficient (measured: >= 16 KB
+        // per input best); whole planes when planes are that large; <= kMaxChunks
+        const int64_t env = env_int("IABN_FUSED_CHUNK", 0);
+        int64_t cv;
+        if (env > 0) {
+            cv = env;
+        } else if (by_plane) {
+            const int64_t per = std::max<int64_t>(1, (1024 + pv - 1) / pv);  // planes per chunk
+            cv = pv * per;
+        } else {
+            cv = 2048 / nin;
+        }
+        cv = std::max<int64_t>(cv, (cap + kMaxChunks - 1) / kMaxChunks);
+        best.chunk_vecs = (uint32_t)std::min<int64_t>(cv, cap);
+        return true;
+    };
+    if (kforce || nforce) {
+        for (int K = kforce ? kforce : 1; K <= (kforce ? kforce : kMaxCluster) && K <= mv; ++K)
+            for (int nb = nforce ? nforce : kMaxBuf; nb >= (nforce ? nforce : 1); --nb)
+                if (consider(K, nb)) goto done;
+        goto done;
+    }
+    for (int K = 1; K <= 8 && K <= mv; ++K)
+        if (consider(K, 2)) goto done;
+    for (int K = 1; K <= kMaxCluster && K <= mv; ++K)
+        if (consider(K, 1)) goto done;
+done:
+    if (best.ok && env_int("IABN_VERBOSE", 0)) {
+        static std::mutex pm;
+        static int printed = 0;
+        std::lock_guard<std::mutex> lk(pm);
+        if (printed++ < 16)
+            fprintf(stderr, "[iabn] fused pass=%d C=%lld m=%lld: K=%d nbuf=%d clusters=%d smem=%zu cap=%u chunk=%u\n",
+                    pass, (long long)g.C, (long long)g.m, best.K, best.nbuf, best.clusters, best.smem,
+                    best.cap, best.chunk_vecs);
+    }
+    return best;
 }
 
 FastDiv fd32(int64_t d) { return make_fastdiv((uint32_t)d); }
 
 template <typename T>
-iabn_status launch_fused(int pass, const FusedPlan& p, const FusedArgs& a, int64_t C,
-                         cudaStream_t st) {
+iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t st) {
+    a.cap = p.cap;
+    a.chunk_vecs = p.chunk_vecs;
+    a.nbuf = (uint32_t)p.nbuf;
+    a.debug = (uint32_t)env_int("IABN_FUSED_DEBUG", 0);
+    a.trace = nullptr;
+    a.trace_ch = 0;
+    if (a.debug & 4u) {  // experiments only: phase timestamps, dumped by iabn_debug_trace
+        static unsigned long long* buf = nullptr;
+        static size_t cap = 0;
+        const uint32_t per = (uint32_t)((a.C + p.clusters - 1) / p.clusters);
+        const size_t need = (size_t)p.clusters * p.K * per * 8;
+        if (need > cap) {
+            if (buf) cudaFree(buf);
+            cudaMalloc(&buf, need * sizeof(unsigned long long));
+            cap = need;
+        }
+        cudaMemsetAsync(buf, 0, need * sizeof(unsigned long long), st);
+        a.trace = buf;
+        a.trace_ch = per;
+        g_trace = buf;
+        g_trace_n = need;
+        g_trace_ch = per;
+    }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(C * p.K), 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.gridDim = dim3((unsigned)(p.clusters * p.K), 1, 1);
+    cfg.blockDim = dim3(kFusedThreads, 1, 1);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -318,14 +406,14 @@ iabn_status launch_fused(int pass, const FusedPlan& p, const FusedArgs& a, int64
     cfg.numAttrs = 1;
     cudaError_t e;
     if (pass == 0)
-        e = cudaLaunchKernelEx(&cfg, fused_fwd_kernel<T>, a);
+        e = cudaLaunchKernelEx(&cfg, fused_kernel<T, 0>, a);
     else
-        e = cudaLaunchKernelEx(&cfg, fused_bwd_kernel<T>, a);
+        e = cudaLaunchKernelEx(&cfg, fused_kernel<T, 1>, a);
     if (e != cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return fail(IABN_ERR_CUDA, "fused launch: %s", cudaGetErrorString(e));
     }
-    return check_launch(pass == 0 ? "fused_fwd_kernel" : "fused_bwd_kernel");
+    return check_launch(pass == 0 ? "fused_kernel<fwd>" : "fused_kernel<bwd>");
 }
 
 // ====================================================================== streaming launches
@@ -630,13 +718,12 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         a.HW = c.g.HW;
         a.m = (uint32_t)c.g.m;
         a.fd_hw = fd32(c.g.HW);
-        a.chunk_vecs = p.chunk_vecs;
         a.momentum = momentum;
         a.eps = eps;
         a.slope = slope;
         a.inv_slope = 1.0f / slope;
         a.flags = flags;
-        return launch_fused<T>(0, p, a, c.g.C, c.st);
+        return launch_fused<T>(0, p, a, c.st);
     }
     IABN_TRY(fwd_stream_stats<T>(c, x));
     return fwd_from_partials<T>(c, wsp<double>(c, c.w.part), c.S, x, z, gamma, beta, rm, rv, sm,
@@ -677,12 +764,11 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
         a.HW = c.g.HW;
         a.m = (uint32_t)c.g.m;
         a.fd_hw = fd32(c.g.HW);
-        a.chunk_vecs = p.chunk_vecs;
         a.eps = eps;
         a.slope = slope;
         a.inv_slope = 1.0f / slope;
         a.flags = flags;
-        return launch_fused<T>(1, p, a, c.g.C, c.st);
+        return launch_fused<T>(1, p, a, c.st);
     }
     double* part = wsp<double>(c, c.w.part);
     IABN_TRY(launch_bwd_reduce<T>(c.g, c.S, z, dz, gamma, beta, eps, slope, flags, part, c.st));
@@ -717,6 +803,16 @@ const char* iabn_status_string(iabn_status s) {
 const char* iabn_last_error(void) { return g_err.c_str(); }
 
 uint64_t iabn_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+// Experiments only (not in include/iabn.h): copy the phase trace of the last fused
+// launch (IABN_FUSED_DEBUG & 4) to host memory; returns the number of values.
+IABN_API size_t iabn_debug_trace(unsigned long long* host, size_t n) {
+    if (!g_trace) return 0;
+    const size_t k = n < g_trace_n ? n : g_trace_n;
+    if (host && k) cudaMemcpy(host, g_trace, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    return g_trace_n;
+}
+IABN_API uint32_t iabn_debug_trace_channels(void) { return g_trace_ch; }
 
 size_t iabn_workspace_bytes(const iabn_desc* desc) {
     Geom g;

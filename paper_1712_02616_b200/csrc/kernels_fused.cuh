@@ -1,17 +1,30 @@
 // kernels_fused.cuh -- channel-resident schedule (NCHW, HW*b a multiple of 16 B).
 //
-// One thread-block CLUSTER of K CTAs owns one channel c.  CTA r of the cluster
-// owns the channel-space slice [lo_r, hi_r) of the channel's m = N*HW values
-// (planes n of HW contiguous values, stride C*HW), which it pulls into shared
-// memory with TMA bulk copies (cp.async.bulk, one mbarrier per ~chunk so the
-// reduction starts on the first chunk while later ones are in flight).  The
-// per-channel reduction is a CTA tree followed by a DSMEM exchange of the K
-// partial records (fixed order => deterministic, identical in every CTA); the
-// apply pass then reads the slice from shared memory and writes the result with
-// 16-byte stores.  HBM traffic is the minimum the method allows:
-//   forward  FF: read x once, write z once                 = 2*E*b
-//   backward BF: read z and dz once, write dx once          = 3*E*b
-// (vs 3*E*b and 5*E*b for kernels_stream.cuh).
+// A persistent grid of thread-block CLUSTERS of K CTAs (K chosen so clusters
+// pack onto the GPCs).  Cluster q owns channels c = q, q + Q, ...; CTA r of the
+// cluster owns the same channel-space slice [lo_r, hi_r) of each of them (the m
+// = N*HW values of a channel are N planes of HW contiguous values, plane stride
+// C*HW).  Each CTA is a warp-specialised pipeline:
+//
+//   producer warp : TMA bulk copies (cp.async.bulk, SASS UBLKCP) of slice t
+//                   into slab buffer t % nbuf of a shared-memory ring, one
+//                   mbarrier per chunk ("full");
+//   reduce warps  : fp32x2 partial sums (FFMA2/FADD2) over the resident slice,
+//                   fp64 CTA record, PUSHED into every peer's shared memory
+//                   (DSMEM st.shared::cluster + remote mbarrier arrive);
+//   exchange warp : waits for the K records of channel s in its own shared
+//                   memory, folds them in rank order (deterministic, identical
+//                   in every CTA), derives the apply coefficients;
+//   apply warps   : outputs of channel s from the still-resident slice with
+//                   16-byte stores, then free the slab buffer ("empty").
+//
+// The exchange never touches L2, so a slice stays in shared memory only for
+// load latency + one DSMEM round trip (Little's law: that residence time,
+// times the HBM rate, is the shared memory the pipeline needs).
+//
+// HBM traffic is the minimum the method allows (vs 3*E*b / 5*E*b streaming):
+//   forward  (PASS 0): read x once, write z once          = 2*E*b
+//   backward (PASS 1): read z and dz once, write dx once   = 3*E*b
 #pragma once
 
 #include "common.cuh"
@@ -19,7 +32,10 @@
 
 namespace iabn {
 
-constexpr int kMaxChunks = 48;
+constexpr int kMaxChunks = 16;  // chunks (mbarriers) per slab buffer
+constexpr int kMaxBuf = 4;      // slab buffers per CTA (ring)
+constexpr int kMaxCluster = 16; // CTAs per cluster (non-portable size above 8)
+constexpr int kSlots = 4;       // in-flight channel records per CTA
 
 struct FusedArgs {
     const void* in0;  // forward: x; backward: z
@@ -34,244 +50,438 @@ struct FusedArgs {
     float* dgamma;
     float* dbeta;
     int64_t C, HW;
-    uint32_t m;  // values per channel
+    uint32_t m;           // values per channel
     FastDiv fd_hw;
-    uint32_t chunk_vecs;  // 16-byte vectors per chunk (per input)
+    uint32_t cap;         // 16-byte vectors reserved per input per buffer (>= slice)
+    uint32_t chunk_vecs;  // vectors per chunk (per input)
+    uint32_t nbuf;        // slab buffers in the ring (2..kMaxBuf)
     float momentum, eps, slope, inv_slope;
     uint32_t flags;
+    uint32_t debug;  // experiments only (IABN_FUSED_DEBUG): 2 = skip the output stores,
+                     // 4 = record phase timestamps into `trace`
+    unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
+    uint32_t trace_ch;          // channels per CTA recorded
 };
 
-// Slice of the channel owned by cluster rank r of K, in 16-byte vectors.
-__device__ __forceinline__ void cta_slice(uint32_t mv, uint32_t r, uint32_t K, uint32_t& vlo,
-                                          uint32_t& vhi) {
-    vlo = (uint32_t)((uint64_t)mv * r / K);
-    vhi = (uint32_t)((uint64_t)mv * (r + 1) / K);
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// phase timestamps (debug & 4): 0 producer issued chunk 0, 1 producer issued last chunk,
+// 2 reduce got chunk 0, 3 reduce got last chunk, 4 record pushed, 5 exchange gathered,
+// 6 apply start, 7 apply end
+#define IABN_TRACE(a, t, slot)                                                          \
+    do {                                                                                \
+        if (((a).debug & 4u) && (t) < (a).trace_ch)                                    \
+            (a).trace[((size_t)blockIdx.x * (a).trace_ch + (t)) * 8 + (slot)] = gtimer(); \
+    } while (0)
+
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+// arrive on a (possibly remote) mbarrier of this cluster; release orders this
+// thread's prior DSMEM stores before the arrival
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+                 : "memory");
+}
+// wait with cluster-scope acquire: peers' DSMEM stores before their arrivals are visible
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1, %2;\n\t"
+        "@!P bra WAITC_%=;\n}" ::"r"(smem_addr(bar)),
+        "r"(parity), "n"(0x100000)
+        : "memory");
 }
 
-// Thread 0: arm chunk barriers and issue the bulk copies of `nin` inputs for
-// channel-space vectors [vlo, vhi) into consecutive smem regions of nv vectors.
-template <typename T>
-__device__ __forceinline__ void issue_loads(const FusedArgs& a, int64_t c, uint32_t vlo,
-                                            uint32_t vhi, uint4* smem, uint64_t* bars,
-                                            int nchunks, int nin) {
-    constexpr int V = Elem<T>::kVec;
-    const uint32_t nv = vhi - vlo;
-    const uint32_t hw = (uint32_t)a.HW;
-    const T* src[2] = {(const T*)a.in0, (const T*)a.in1};
-    for (int k = 0; k < nchunks; ++k) {
-        const uint32_t c_lo = vlo + k * a.chunk_vecs;
-        const uint32_t c_hi = min(vhi, c_lo + a.chunk_vecs);
-        mbar_arrive_expect_tx(&bars[k], (c_hi - c_lo) * 16u * nin);
-        uint32_t j = c_lo * V;  // channel-space element
-        const uint32_t jend = c_hi * V;
-        while (j < jend) {
-            const uint32_t n = j / hw, s = j - n * hw;
-            const uint32_t len = min(jend - j, hw - s);
-            const int64_t goff = ((int64_t)n * a.C + c) * a.HW + s;
-            for (int i = 0; i < nin; ++i)
-                bulk_g2s(smem + (size_t)i * nv + (j / V - vlo), src[i] + goff,
-                         len * (uint32_t)sizeof(T), &bars[k]);
-            j += len;
-        }
+// Slice of a channel owned by rank r of K, in 16-byte vectors: whole planes when
+// there are at least K planes (each plane is then one bulk copy), else an even
+// split of the channel's vectors.
+__device__ __forceinline__ void cta_slice(uint32_t mv, uint32_t pv, uint32_t r, uint32_t K,
+                                          uint32_t& vlo, uint32_t& vhi) {
+    const uint32_t np = mv / pv;  // planes (N)
+    if (np >= K) {
+        vlo = pv * (uint32_t)((uint64_t)np * r / K);
+        vhi = pv * (uint32_t)((uint64_t)np * (r + 1) / K);
+    } else {
+        vlo = (uint32_t)((uint64_t)mv * r / K);
+        vhi = (uint32_t)((uint64_t)mv * (r + 1) / K);
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads) fused_fwd_kernel(const FusedArgs a) {
+// Per-channel constants of the apply pass (shared memory).
+struct ApplyCoef {
+    float2 P;   // forward: (A, A) ;           backward: z >= 0 branch (alpha, kappa)
+    float2 Q;   // forward: (B', B') ;         backward: z < 0 branch (alpha a, kappa / a)
+    float mu;   // forward: mu_hi ;            backward: cc
+};
+
+#ifndef IABN_REDUCE_WARPS
+#define IABN_REDUCE_WARPS 8
+#endif
+#ifndef IABN_APPLY_WARPS
+#define IABN_APPLY_WARPS 8
+#endif
+constexpr int kReduceWarps = IABN_REDUCE_WARPS;  // stream each resident slice for the channel sums
+constexpr int kApplyWarps = IABN_APPLY_WARPS;    // stream it again, one channel behind, for outputs
+constexpr int kExchangeWarp = kReduceWarps + kApplyWarps;  // folds the group's records
+constexpr int kProducerWarp = kExchangeWarp + 1;           // issues the TMA bulk copies
+constexpr int kFusedThreads = (kProducerWarp + 1) * 32;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void reducer_sync() {  // named barrier over the reduce warps
+    asm volatile("bar.sync 1, %0;" ::"n"(kReduceWarps * 32) : "memory");
+}
+__device__ __forceinline__ void applier_sync() {  // named barrier over the apply warps
+    asm volatile("bar.sync 2, %0;" ::"n"(kApplyWarps * 32) : "memory");
+}
+// One warp of a group polls the mbarrier; the rest block on a named barrier (no
+// issue slots burnt by a whole group of waiting warps).
+template <int GROUP>
+__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool leader) {
+    if (leader) mbar_wait(bar, parity);
+    if (GROUP == 1)
+        reducer_sync();
+    else
+        applier_sync();
+}
+
+template <typename T, int PASS>
+__global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedArgs a) {
+    constexpr int NIN = PASS == 0 ? 1 : 2;
+    constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
     constexpr int V = Elem<T>::kVec;
+    constexpr int NP = Pairs<T>::kN;
     extern __shared__ __align__(128) uint4 smem[];
-    __shared__ __align__(8) uint64_t bars[kMaxChunks];
-    __shared__ double red[2 * kThreads / 32];
-    __shared__ double part[3];
-    __shared__ float4 coef_s;
+    __shared__ __align__(8) uint64_t full[kMaxBuf][kMaxChunks];  // TMA -> reduce and apply warps
+    __shared__ __align__(8) uint64_t empty[kMaxBuf][kMaxChunks]; // apply warps -> producer
+    __shared__ __align__(8) uint64_t gathered[kSlots];           // K peers' records arrived
+    __shared__ __align__(8) uint64_t slotfree[kSlots];           // K peers folded my record slot
+    __shared__ __align__(8) uint64_t ready[2];                   // exchange -> apply warps
+    __shared__ __align__(8) uint64_t freed[2];                   // apply warps -> exchange
+    __shared__ double rec[kSlots][kMaxCluster][NR];              // pushed by the K peers
+    __shared__ double red[2][2][kReduceWarps];
+    __shared__ ApplyCoef cs[2];
 
     const uint32_t K = cluster_nctarank(), r = cluster_ctarank();
-    const int64_t c = blockIdx.x / K;
+    const uint32_t q = blockIdx.x / K, Q = gridDim.x / K;
+    const uint32_t nbuf = a.nbuf;
+    const uint32_t C = (uint32_t)a.C;
+    const uint32_t nT = q < C ? (C - q + Q - 1) / Q : 0;  // channels of this cluster
     uint32_t vlo, vhi;
-    cta_slice(a.m / V, r, K, vlo, vhi);
+    cta_slice(a.m / V, (uint32_t)a.HW / V, r, K, vlo, vhi);
     const uint32_t nv = vhi - vlo;
-    const int nchunks = (int)((nv + a.chunk_vecs - 1) / a.chunk_vecs);
+    const int nch = (int)((nv + a.chunk_vecs - 1) / a.chunk_vecs);
+    const size_t bufv = (size_t)NIN * a.cap;  // vectors per slab buffer
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        for (int k = 0; k < nchunks; ++k) mbar_init(&bars[k], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) issue_loads<T>(a, c, vlo, vhi, smem, bars, nchunks, 1);
-
-    // ---- F1: shifted fp32 chains over the resident slice, fp64 combine
-    float a1[V], a2[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
-    double d1 = 0.0, d2 = 0.0;
-    float K0 = 0.f;
-    if (nchunks > 0) {
-        mbar_wait(&bars[0], 0);
-        float f[V];
-        unpack<T>(smem[0], f);
-        K0 = f[0];
-    }
-    for (int k = 0; k < nchunks; ++k) {
-        mbar_wait(&bars[k], 0);
-        const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-        for (uint32_t v = c_lo + threadIdx.x; v < c_hi; v += kThreads) {
-            float f[V];
-            unpack<T>(smem[v], f);
-#pragma unroll
-            for (int q = 0; q < V; ++q) {
-                const float dv = f[q] - K0;
-                a1[q] += dv;
-                a2[q] = fmaf(dv, dv, a2[q]);
+        for (uint32_t b = 0; b < nbuf; ++b) {
+            for (int k = 0; k < nch; ++k) {
+                mbar_init(&full[b][k], 1);
+                mbar_init(&empty[b][k], kApplyWarps);
             }
         }
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-            d1 += a1[q];
-            d2 += a2[q];
-            a1[q] = a2[q] = 0.f;
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(&gathered[i], K);
+            mbar_init(&slotfree[i], K);
         }
-    }
-    double v2[2] = {d1, d2};
-    block_sum<2>(v2, red);
-    if (threadIdx.x == 0) write_raw_moments(part, (double)nv * V, (double)K0, v2[0], v2[1]);
-
-    // ---- cluster exchange of the K partial records (DSMEM)
-    cluster_arrive_release();
-    cluster_wait_acquire();
-    if (threadIdx.x == 0) {
-        double cnt = 0.0, sum = 0.0, sumsq = 0.0;
-        for (uint32_t q = 0; q < K; ++q) {
-            cnt += ld_dsmem_f64(&part[0], q);
-            sum += ld_dsmem_f64(&part[1], q);
-            sumsq += ld_dsmem_f64(&part[2], q);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&ready[i], 1);
+            mbar_init(&freed[i], kApplyWarps);
         }
-        double mean, var;
-        coef_s = fwd_coef_from_moments(cnt, sum, sumsq, a.gamma[c], a.beta[c], a.eps, a.flags,
-                                       &mean, &var);
-        if (r == 0) {
-            a.save_mean[c] = (float)mean;
-            a.save_var[c] = (float)var;
-            update_running(a.running_mean, a.running_var, c, mean, var, cnt, a.momentum, a.flags);
-        }
-    }
-    __syncthreads();
-    cluster_arrive_release();  // this CTA no longer reads remote shared memory
-
-    // ---- F2: z = f(x A + B) from shared memory, 16-byte stores (z may be x)
-    const float4 cf = coef_s;
-    const float slope = a.slope;
-    T* z = (T*)a.out;
-    const uint32_t hw = (uint32_t)a.HW;
-    for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
-        float f[V];
-        unpack<T>(smem[v], f);
-#pragma unroll
-        for (int q = 0; q < V; ++q) f[q] = leaky(affine(f[q], cf), slope);
-        const uint32_t j = (vlo + v) * V;
-        const uint32_t n = fdiv(j, a.fd_hw);
-        st_vec(z + ((int64_t)n * a.C + c) * a.HW + (j - n * hw), pack<T>(f));
-    }
-    cluster_wait_acquire();  // peers are done reading this CTA's part[]
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads) fused_bwd_kernel(const FusedArgs a) {
-    constexpr int V = Elem<T>::kVec;
-    extern __shared__ __align__(128) uint4 smem[];
-    __shared__ __align__(8) uint64_t bars[kMaxChunks];
-    __shared__ double red[2 * kThreads / 32];
-    __shared__ double part[2];
-    __shared__ float4 coef_s;
-
-    const uint32_t K = cluster_nctarank(), r = cluster_ctarank();
-    const int64_t c = blockIdx.x / K;
-    uint32_t vlo, vhi;
-    cta_slice(a.m / V, r, K, vlo, vhi);
-    const uint32_t nv = vhi - vlo;
-    const int nchunks = (int)((nv + a.chunk_vecs - 1) / a.chunk_vecs);
-    const uint4* zs = smem;
-    const uint4* ds = smem + nv;
-
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < nchunks; ++k) mbar_init(&bars[k], 1);
         fence_mbar_init();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) issue_loads<T>(a, c, vlo, vhi, smem, bars, nchunks, 2);
-
-    const InvAffine ia = inv_affine(a.gamma[c], a.beta[c], a.eps, a.flags);
-    const float slope = a.slope, inv_slope = a.inv_slope;
-
-    // ---- B1: S1 = sum dy, S2 = sum dy x^ over the resident slice
-    float a1[V], a2[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
-    double d1 = 0.0, d2 = 0.0;
-    for (int k = 0; k < nchunks; ++k) {
-        mbar_wait(&bars[k], 0);
-        const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-        for (uint32_t v = c_lo + threadIdx.x; v < c_hi; v += kThreads) {
-            float fz[V], fd[V];
-            unpack<T>(zs[v], fz);
-            unpack<T>(ds[v], fd);
-#pragma unroll
-            for (int q = 0; q < V; ++q) {
-                float dy, xh;
-                grad_terms(fz[q], fd[q], slope, inv_slope, ia, dy, xh);
-                a1[q] += dy;
-                a2[q] = fmaf(dy, xh, a2[q]);
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-            d1 += a1[q];
-            d2 += a2[q];
-            a1[q] = a2[q] = 0.f;
-        }
-    }
-    double v2[2] = {d1, d2};
-    block_sum<2>(v2, red);
-    if (threadIdx.x == 0) {
-        part[0] = v2[0];
-        part[1] = v2[1];
-    }
+    // every CTA's barriers are initialised before any peer may arrive on them
     cluster_arrive_release();
     cluster_wait_acquire();
-    if (threadIdx.x == 0) {
-        double S1 = 0.0, S2 = 0.0;
-        for (uint32_t q = 0; q < K; ++q) {
-            S1 += ld_dsmem_f64(&part[0], q);
-            S2 += ld_dsmem_f64(&part[1], q);
-        }
-        coef_s = bwd_coef_from_sums(S1, S2, (double)a.m, a.gamma[c], a.beta[c], a.save_var[c],
-                                    a.eps, a.flags);
-        if (r == 0) {
-            a.dbeta[c] = (float)S1;
-            a.dgamma[c] = (float)(gamma_sign(a.gamma[c], a.flags) * S2);
-        }
-    }
-    __syncthreads();
-    cluster_arrive_release();
 
-    // ---- B2: dx = alpha dy + kappa y + cc (dx may be dz: this CTA's dz slice is resident)
-    const float4 cf = coef_s;
-    T* dx = (T*)a.out;
-    const uint32_t hw = (uint32_t)a.HW;
-    for (uint32_t v = threadIdx.x; v < nv; v += kThreads) {
-        float fz[V], fd[V];
-        unpack<T>(zs[v], fz);
-        unpack<T>(ds[v], fd);
+    if (warp == kProducerWarp) {
+        // ================================================ producer: slab t into buffer t % nbuf,
+        // chunk by chunk: chunk k is refilled as soon as the apply warps released it
+        if (lane == 0) {
+            const T* src[2] = {(const T*)a.in0, (const T*)a.in1};
+            const uint32_t hw = (uint32_t)a.HW;
+            for (uint32_t t = 0; t < nT; ++t) {
+                const uint32_t b = t % nbuf;
+                const int64_t c = q + t * Q;
+                uint4* buf = smem + b * bufv;
+                for (int k = 0; k < nch; ++k) {
+                    if (t >= nbuf) {
+                        mbar_wait(&empty[b][k], (t / nbuf - 1) & 1u);  // chunk k of t - nbuf applied
+                        fence_proxy_async_smem();  // generic-proxy reads before the async refill
+                    }
+                    const uint32_t c_lo = vlo + k * a.chunk_vecs;
+                    const uint32_t c_hi = min(vhi, c_lo + a.chunk_vecs);
+                    if (k == 0) IABN_TRACE(a, t, 0);
+                    if (k == nch - 1) IABN_TRACE(a, t, 1);
+                    mbar_arrive_expect_tx(&full[b][k], (c_hi - c_lo) * 16u * NIN);
+                    uint32_t j = c_lo * V;  // channel-space element
+                    const uint32_t jend = c_hi * V;
+                    uint32_t n = fdiv(j, a.fd_hw);
+                    uint32_t sp = j - n * hw;
+                    while (j < jend) {
+                        const uint32_t len = min(jend - j, hw - sp);
+                        const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
 #pragma unroll
-        for (int q = 0; q < V; ++q) {
-            const bool pos = fz[q] >= 0.f;
-            const float y = pos ? fz[q] : fz[q] * inv_slope;
-            const float dy = pos ? fd[q] : fd[q] * slope;
-            fz[q] = fmaf(cf.x, dy, fmaf(cf.y, y, cf.z));
+                        for (int i = 0; i < NIN; ++i)
+                            bulk_g2s(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
+                                     len * (uint32_t)sizeof(T), &full[b][k]);
+                        j += len;
+                        ++n;
+                        sp = 0;
+                    }
+                }
+            }
         }
-        const uint32_t j = (vlo + v) * V;
-        const uint32_t n = fdiv(j, a.fd_hw);
-        st_vec(dx + ((int64_t)n * a.C + c) * a.HW + (j - n * hw), pack<T>(fz));
+        __syncwarp();
+    } else if (warp == kExchangeWarp) {
+        // ================================================ exchange: fold the K records of each
+        // channel in rank order (bit-identical in all K CTAs)
+        for (uint32_t s = 0; s < nT; ++s) {
+            const int64_t cp = q + s * Q;
+            const uint32_t slot = s & 1u, rs = s % kSlots;
+            if (s >= 2) mbar_wait(&freed[slot], (s / 2 - 1) & 1u);
+            mbar_wait_cluster(&gathered[rs], (s / kSlots) & 1u);
+            if (lane == 0) IABN_TRACE(a, s, 5);
+            if (lane == 0) {
+                double v[NR];
+#pragma unroll
+                for (int k = 0; k < NR; ++k) v[k] = 0.0;
+                for (uint32_t j = 0; j < K; ++j)
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) v[k] += rec[rs][j][k];
+                if (PASS == 0) {
+                    double mean, var;
+                    const float4 f = fwd_coef_from_moments(v[0], v[1], v[2], a.gamma[cp],
+                                                           a.beta[cp], a.eps, a.flags, &mean, &var);
+                    // y = ((x - mu_hi) - mu_lo) A + beta = (x - mu_hi) A + (beta - mu_lo A)
+                    const float Bp = (float)((double)f.w - (double)f.z * (double)f.x);
+                    cs[slot].P = make_float2(f.x, f.x);
+                    cs[slot].Q = make_float2(Bp, Bp);
+                    cs[slot].mu = f.y;
+                    if (r == 0) {
+                        a.save_mean[cp] = (float)mean;
+                        a.save_var[cp] = (float)var;
+                        update_running(a.running_mean, a.running_var, cp, mean, var, v[0],
+                                       a.momentum, a.flags);
+                    }
+                } else {
+                    const float4 f = bwd_coef_from_sums(v[0], v[1], (double)a.m, a.gamma[cp],
+                                                        a.beta[cp], a.save_var[cp], a.eps, a.flags);
+                    // dx = alpha dy + kappa y + cc with dy, y on the branch of sign(z):
+                    //   z >= 0: alpha dz + kappa z + cc;  z < 0: (alpha a) dz + (kappa / a) z + cc
+                    cs[slot].P = make_float2(f.x, f.y);
+                    cs[slot].Q = make_float2(f.x * a.slope, f.y * a.inv_slope);
+                    cs[slot].mu = f.z;
+                    if (r == 0) {
+                        a.dbeta[cp] = (float)v[0];
+                        a.dgamma[cp] = (float)(gamma_sign(a.gamma[cp], a.flags) * v[1]);
+                    }
+                }
+                mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
+            }
+            __syncwarp();
+            // the slot of every peer that pushed into me may be reused by it
+            if (lane < K) mbar_arrive_cluster(mapa(&slotfree[rs], lane));
+        }
+    } else if (warp < kReduceWarps) {
+        // ================================================ reduce warps: channel sums over the
+        // resident slice; the CTA record is pushed into all K peers (DSMEM)
+        constexpr int RT = kReduceWarps * 32;
+        for (uint32_t t = 0; t < nT; ++t) {
+            const int64_t c = q + t * Q;
+            const uint32_t b = t % nbuf, par = (t / nbuf) & 1u;
+            const uint4* xs = smem + b * bufv;  // x (fwd) or z (bwd)
+            const uint4* ds = xs + a.cap;       // dz (bwd)
+            float2 s1[NP], s2[NP];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) s1[i] = s2[i] = make_float2(0.f, 0.f);
+            float K0 = 0.f;
+            float2 ig2 = make_float2(0.f, 0.f), nb2 = ig2;
+            if (PASS == 0) {
+                group_wait<1>(&full[b][0], par, warp == 0);
+                float2 p0[NP];
+                Pairs<T>::load(xs[0], p0);
+                K0 = p0[0].x;  // shift: a sample of this slice (cancellation-free variance)
+            } else {
+                const InvAffine ia = inv_affine(__ldg(a.gamma + c), __ldg(a.beta + c), a.eps, a.flags);
+                ig2 = make_float2(ia.inv_g, ia.inv_g);
+                nb2 = make_float2(ia.nb, ia.nb);
+            }
+            auto reduce_vec = [&](const uint32_t v) {
+                if (PASS == 0) {
+                    float2 d[NP];
+                    Pairs<T>::load_sub(xs[v], K0, d);
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) {
+                        s1[i] = add2(s1[i], d[i]);
+                        s2[i] = fma2(d[i], d[i], s2[i]);
+                    }
+                } else {
+                    // Alg. 2 l.2-5: dy = f'(z) dz; dy x^ = dy (y inv_g + nb) and dy y = dz z
+                    // (f' f^-1 is the identity on each branch), so per element
+                    // dy x^ = (dz z) inv_g + nb dy  (variant I: per-element products).
+                    float2 zz[NP], dd[NP];
+                    Pairs<T>::load(xs[v], zz);
+                    Pairs<T>::load(ds[v], dd);
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) {
+                        const float2 sel = make_float2(zz[i].x >= 0.f ? 1.f : a.slope,
+                                                       zz[i].y >= 0.f ? 1.f : a.slope);
+                        const float2 dy = mul2(dd[i], sel);
+                        const float2 p = mul2(dd[i], zz[i]);
+                        s1[i] = add2(s1[i], dy);
+                        s2[i] = add2(s2[i], fma2(p, ig2, mul2(dy, nb2)));
+                    }
+                }
+            };
+            for (int k = 0; k < nch; ++k) {
+                if (PASS == 1 || k > 0) group_wait<1>(&full[b][k], par, warp == 0);
+                if (threadIdx.x == 0 && k == 0) IABN_TRACE(a, t, 2);
+                if (threadIdx.x == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
+                const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+                uint32_t v = c_lo + threadIdx.x;
+                for (; v + 3 * RT < c_hi; v += 4 * RT) {
+                    reduce_vec(v);
+                    reduce_vec(v + RT);
+                    reduce_vec(v + 2 * RT);
+                    reduce_vec(v + 3 * RT);
+                }
+                for (; v < c_hi; v += RT) reduce_vec(v);
+            }
+            double d1 = 0.0, d2 = 0.0;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                d1 += (double)s1[i].x + (double)s1[i].y;
+                d2 += (double)s2[i].x + (double)s2[i].y;
+            }
+            d1 = warp_sum(d1);
+            d2 = warp_sum(d2);
+            if (lane == 0) {
+                red[t & 1][0][warp] = d1;
+                red[t & 1][1][warp] = d2;
+            }
+            reducer_sync();
+            if (warp == 0) {
+                double S1 = 0.0, S2 = 0.0;
+                for (int w = 0; w < kReduceWarps; ++w) {
+                    S1 += red[t & 1][0][w];
+                    S2 += red[t & 1][1][w];
+                }
+                double out[NR];
+                if (PASS == 0) {
+                    write_raw_moments(out, (double)nv * V, (double)K0, S1, S2);
+                } else {
+                    out[0] = S1;
+                    out[1] = S2;
+                }
+                const uint32_t rs = t % kSlots;
+                // my record slot rs in every peer must have been folded (channel t - kSlots)
+                if (t >= (uint32_t)kSlots) mbar_wait_cluster(&slotfree[rs], (t / kSlots - 1) & 1u);
+                if (lane < K) {  // lane j pushes this CTA's record into peer j and signals it
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) st_cluster_f64(mapa(&rec[rs][r][k], lane), out[k]);
+                    mbar_arrive_cluster(mapa(&gathered[rs], lane));
+                }
+                if (lane == 0) IABN_TRACE(a, t, 4);
+            }
+        }
+    } else {
+        // ================================================ apply warps: outputs from the resident
+        // slice once the channel's coefficients are in (the reduce warps have read it by then)
+        const uint32_t hw = (uint32_t)a.HW;
+        const float2 sl2 = make_float2(a.slope, a.slope);
+        constexpr int AT = kApplyWarps * 32;
+        const uint32_t at = threadIdx.x - kReduceWarps * 32;
+        T* out = (T*)a.out;
+        const int64_t chw = a.C * a.HW;
+        const uint32_t step = AT * V;
+        const bool step_inc = hw >= step;  // at most one plane boundary per step
+        for (uint32_t s = 0; s < nT; ++s) {
+            const int64_t cp = q + s * Q;
+            const uint32_t b = s % nbuf, slot = s & 1u;
+            group_wait<2>(&ready[slot], (s / 2) & 1u, warp == kReduceWarps);
+            if (at == 0) IABN_TRACE(a, s, 6);
+            const uint4* xs = smem + b * bufv;
+            const uint4* ds = xs + a.cap;
+            const float2 P = cs[slot].P, Q2 = cs[slot].Q;
+            const float mu = cs[slot].mu;
+            // output cursor: plane jn / offset jsp of this thread's current vector; within a
+            // chunk the thread visits v = c_lo + at, + AT, ... (channel-space steps of AT*V)
+            uint32_t jn = 0, jsp = 0;
+            T* const outc = out + cp * a.HW;
+            auto apply_vec = [&](const uint32_t v) {
+                float2 w[NP];
+                if (PASS == 0) {
+                    Pairs<T>::load_sub(xs[v], mu, w);
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) {
+                        const float2 y = fma2(w[i], P, Q2);
+                        const float2 ay = mul2(y, sl2);  // f(y) = max(y, a y) for 0 < a <= 1
+                        w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                    }
+                } else {
+                    float2 dd[NP];
+                    Pairs<T>::load(xs[v], w);
+                    Pairs<T>::load(ds[v], dd);
+                    const float2 cc2 = make_float2(mu, mu);
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) {
+                        const bool px = w[i].x >= 0.f, py = w[i].y >= 0.f;
+                        const float2 al = make_float2(px ? P.x : Q2.x, py ? P.x : Q2.x);
+                        const float2 ka = make_float2(px ? P.y : Q2.y, py ? P.y : Q2.y);
+                        w[i] = fma2(al, dd[i], fma2(ka, w[i], cc2));
+                    }
+                }
+                T* dst = outc + (int64_t)jn * chw + jsp;
+                if (step_inc) {
+                    jsp += step;
+                    if (jsp >= hw) {
+                        jsp -= hw;
+                        ++jn;
+                    }
+                } else {
+                    const uint32_t j = jn * hw + jsp + step;
+                    jn = fdiv(j, a.fd_hw);
+                    jsp = j - jn * hw;
+                }
+                if (!(a.debug & 2u)) st_vec(dst, Pairs<T>::store(w));
+            };
+            for (int k = 0; k < nch; ++k) {
+                const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+                uint32_t v = c_lo + at;
+                {
+                    const uint32_t j0 = (vlo + v) * V;
+                    jn = fdiv(j0, a.fd_hw);
+                    jsp = j0 - jn * hw;
+                }
+                for (; v + 3 * AT < c_hi; v += 4 * AT) {
+                    apply_vec(v);
+                    apply_vec(v + AT);
+                    apply_vec(v + 2 * AT);
+                    apply_vec(v + 3 * AT);
+                }
+                for (; v < c_hi; v += AT) apply_vec(v);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[b][k]);  // chunk k of buffer b may be refilled
+            }
+            if (at == 0) IABN_TRACE(a, s, 7);
+            if (lane == 0) mbar_arrive(&freed[slot]);  // coefficient slot may be rewritten
+        }
     }
+    // peers may still push records / arrive on this CTA's barriers until they finish
+    cluster_arrive_release();
     cluster_wait_acquire();
 }
 

@@ -1,0 +1,4 @@
+timeout 600 python -m pytest tests -m "gpu and not slow" -q -x --timeout 300 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
+B="python bench.py --steps 60 --warmup 5 --e2e-steps 0 --no-cpu-baseline"
+for dbg in 0 1 2 3; do for kb in 100 200; do IABN_FUSED_DEBUG=$dbg IABN_FUSED_SMEM_KB=$kb timeout 300 $B > gpurun_out/e5_d${dbg}_kb$kb.log 2>&1; done; done
+echo done
