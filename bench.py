@@ -65,7 +65,17 @@ def parse():
 
 
 def shard_sizes(N: int, world: int) -> list[int]:
+    """Strong scaling: rank r holds samples [N r / G, N (r+1) / G) of the global batch."""
     return [N * (r + 1) // world - N * r // world for r in range(world)]
+
+
+def max_over_ranks(values, device, dist, world: int) -> list[float]:
+    """Element-wise max of per-rank timings (the slowest rank defines the step)."""
+    import torch
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
 
 
 def load_peak():
@@ -347,10 +357,7 @@ def main():
             total_ms, fwd, bwd, launches = timed()
 
     # max over ranks
-    t = torch.tensor([total_ms, sum(fwd), sum(bwd)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, fwd_sum, bwd_sum = t.tolist()
+    total_ms, fwd_sum, bwd_sum = max_over_ranks([total_ms, sum(fwd), sum(bwd)], dev, dist, world)
     K = args.steps
     ms_per_step = total_ms / K
     bytes_step_all = 5 * E_all * b

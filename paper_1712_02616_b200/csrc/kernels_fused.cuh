@@ -125,7 +125,7 @@ struct ApplyCoef {
 };
 
 #ifndef IABN_REDUCE_WARPS
-#define IABN_REDUCE_WARPS 8
+#define IABN_REDUCE_WARPS 4
 #endif
 #ifndef IABN_APPLY_WARPS
 #define IABN_APPLY_WARPS 8
@@ -157,7 +157,7 @@ __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool 
 }
 
 template <typename T, int PASS>
-__global__ void __launch_bounds__(kFusedThreads) fused_kernel(const FusedArgs a) {
+__global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs a) {
     constexpr int NIN = PASS == 0 ? 1 : 2;
     constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
     constexpr int V = Elem<T>::kVec;

@@ -87,6 +87,19 @@ def _flags(gamma_mode: str, running_var_biased: bool = False, extra: int = 0) ->
     return _GAMMA[gamma_mode] | (L.RUNNING_VAR_BIASED if running_var_biased else 0) | extra
 
 
+def broadcast_unique_id(group, make_id) -> bytes:
+    """Rank 0 of `group` calls make_id(); every rank returns rank 0's 128 bytes."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    obj = [make_id() if rank == 0 else None]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise RuntimeError("bad communicator id")
+    return bytes(uid)
+
+
 @dataclass
 class Comm:
     """NCCL communicator of the synchronized variant (iabn_comm)."""
@@ -110,11 +123,8 @@ class Comm:
     def from_process_group(cls, group=None) -> "Comm":
         """Rank 0 draws the NCCL id; torch.distributed broadcasts it (plumbing)."""
         import torch.distributed as dist
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-        obj = [cls.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0,
-                                   group=group)
-        return cls.create(world, rank, obj[0])
+        uid = broadcast_unique_id(group, cls.unique_id)
+        return cls.create(dist.get_world_size(group), dist.get_rank(group), uid)
 
     def close(self) -> None:
         if self.handle:
