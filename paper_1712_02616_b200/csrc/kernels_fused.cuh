@@ -85,6 +85,15 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_f64(uint32_t addr, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
+// remote asynchronous store of 16 bytes into a peer's shared memory that signals the
+// peer's mbarrier with complete_tx (no release fence on the pushing thread)
+__device__ __forceinline__ void st_async_f64x2(uint32_t addr, double a, double b, uint32_t mbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(
+            addr),
+        "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(mbar)
+        : "memory");
+}
 // arrive on a (possibly remote) mbarrier of this cluster; release orders this
 // thread's prior DSMEM stores before the arrival
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
@@ -169,7 +178,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
     __shared__ __align__(8) uint64_t slotfree[kSlots];           // K peers folded my record slot
     __shared__ __align__(8) uint64_t ready[2];                   // exchange -> apply warps
     __shared__ __align__(8) uint64_t freed[2];                   // apply warps -> exchange
-    __shared__ double rec[kSlots][kMaxCluster][NR];              // pushed by the K peers
+    __shared__ __align__(16) double rec[kSlots][kMaxCluster][4];  // pushed by the K peers
     __shared__ double red[2][2][kReduceWarps];
     __shared__ ApplyCoef cs[2];
 
@@ -193,7 +202,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
             }
         }
         for (int i = 0; i < kSlots; ++i) {
-            mbar_init(&gathered[i], K);
+            mbar_init(&gathered[i], 1);  // own expect_tx; the K records arrive as transactions
             mbar_init(&slotfree[i], K);
         }
         for (int i = 0; i < 2; ++i) {
@@ -248,28 +257,45 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
     } else if (warp == kExchangeWarp) {
         // ================================================ exchange: fold the K records of each
         // channel in rank order (bit-identical in all K CTAs)
+        const double inv_m = 1.0 / (double)a.m;
         for (uint32_t s = 0; s < nT; ++s) {
             const int64_t cp = q + s * Q;
             const uint32_t slot = s & 1u, rs = s % kSlots;
             if (s >= 2) mbar_wait(&freed[slot], (s / 2 - 1) & 1u);
+            constexpr uint32_t RB = NR == 3 ? 32u : 16u;  // record bytes per peer
+            // per-channel terms that do not depend on the records, before the wait
+            double g = 0.0, bet = 0.0, rstd_b = 0.0;
+            if (lane == 0) {
+                g = gamma_eff(a.gamma[cp], a.eps, a.flags);
+                bet = (double)a.beta[cp];
+                if (PASS == 1) rstd_b = rsqrt((double)a.save_var[cp] + (double)a.eps);
+                mbar_arrive_expect_tx(&gathered[rs], K * RB);
+            }
             mbar_wait_cluster(&gathered[rs], (s / kSlots) & 1u);
             if (lane == 0) IABN_TRACE(a, s, 5);
+            // fold: lane j < K takes rank j's record, then a fixed xor tree (the same
+            // order in every CTA of the cluster => bit-identical coefficients)
+            double v[NR];
+#pragma unroll
+            for (int k = 0; k < NR; ++k) v[k] = lane < K ? rec[rs][lane][k] : 0.0;
+#pragma unroll
+            for (int k = 0; k < NR; ++k)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
             if (lane == 0) {
-                double v[NR];
-#pragma unroll
-                for (int k = 0; k < NR; ++k) v[k] = 0.0;
-                for (uint32_t j = 0; j < K; ++j)
-#pragma unroll
-                    for (int k = 0; k < NR; ++k) v[k] += rec[rs][j][k];
                 if (PASS == 0) {
-                    double mean, var;
-                    const float4 f = fwd_coef_from_moments(v[0], v[1], v[2], a.gamma[cp],
-                                                           a.beta[cp], a.eps, a.flags, &mean, &var);
-                    // y = ((x - mu_hi) - mu_lo) A + beta = (x - mu_hi) A + (beta - mu_lo A)
-                    const float Bp = (float)((double)f.w - (double)f.z * (double)f.x);
-                    cs[slot].P = make_float2(f.x, f.x);
+                    // mean, biased var; A = g rstd; y = (x - mu_hi) A + B'
+                    const double mean = v[1] * inv_m;
+                    double var = fma(-mean, mean, v[2] * inv_m);
+                    var = var > 0.0 ? var : 0.0;
+                    const double A = g * rsqrt(var + (double)a.eps);
+                    const float mu_hi = (float)mean;
+                    const double mu_lo = mean - (double)mu_hi;
+                    const float Af = (float)A, Bp = (float)(bet - mu_lo * A);
+                    cs[slot].P = make_float2(Af, Af);
                     cs[slot].Q = make_float2(Bp, Bp);
-                    cs[slot].mu = f.y;
+                    cs[slot].mu = mu_hi;
+                    mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
                     if (r == 0) {
                         a.save_mean[cp] = (float)mean;
                         a.save_var[cp] = (float)var;
@@ -277,19 +303,23 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                                        a.momentum, a.flags);
                     }
                 } else {
-                    const float4 f = bwd_coef_from_sums(v[0], v[1], (double)a.m, a.gamma[cp],
-                                                        a.beta[cp], a.save_var[cp], a.eps, a.flags);
-                    // dx = alpha dy + kappa y + cc with dy, y on the branch of sign(z):
+                    // dx = alpha dy + kappa y + cc (PAPER.md:168 refolded in y):
+                    //   alpha = g rstd, kappa = -rstd S2/m, cc = rstd (S2 beta - g S1)/m
+                    // with dy, y on the branch of sign(z):
                     //   z >= 0: alpha dz + kappa z + cc;  z < 0: (alpha a) dz + (kappa / a) z + cc
-                    cs[slot].P = make_float2(f.x, f.y);
-                    cs[slot].Q = make_float2(f.x * a.slope, f.y * a.inv_slope);
-                    cs[slot].mu = f.z;
+                    const double rm = rstd_b * inv_m;
+                    const float alpha = (float)(g * rstd_b);
+                    const float kappa = (float)(-rm * v[1]);
+                    const float cc = (float)(rm * fma(v[1], bet, -g * v[0]));
+                    cs[slot].P = make_float2(alpha, kappa);
+                    cs[slot].Q = make_float2(alpha * a.slope, kappa * a.inv_slope);
+                    cs[slot].mu = cc;
+                    mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
                     if (r == 0) {
                         a.dbeta[cp] = (float)v[0];
                         a.dgamma[cp] = (float)(gamma_sign(a.gamma[cp], a.flags) * v[1]);
                     }
                 }
-                mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
             }
             __syncwarp();
             // the slot of every peer that pushed into me may be reused by it
@@ -389,10 +419,10 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 const uint32_t rs = t % kSlots;
                 // my record slot rs in every peer must have been folded (channel t - kSlots)
                 if (t >= (uint32_t)kSlots) mbar_wait_cluster(&slotfree[rs], (t / kSlots - 1) & 1u);
-                if (lane < K) {  // lane j pushes this CTA's record into peer j and signals it
-#pragma unroll
-                    for (int k = 0; k < NR; ++k) st_cluster_f64(mapa(&rec[rs][r][k], lane), out[k]);
-                    mbar_arrive_cluster(mapa(&gathered[rs], lane));
+                if (lane < K) {  // lane j pushes this CTA's record into peer j (st.async)
+                    const uint32_t mb = mapa(&gathered[rs], lane);
+                    st_async_f64x2(mapa(&rec[rs][r][0], lane), out[0], out[1], mb);
+                    if (NR == 3) st_async_f64x2(mapa(&rec[rs][r][2], lane), out[NR - 1], 0.0, mb);
                 }
                 if (lane == 0) IABN_TRACE(a, t, 4);
             }
