@@ -94,10 +94,12 @@ __device__ __forceinline__ uint4 ld_vec(const void* p) {
                  : "l"(p));
     return r;
 }
+// (no "memory" clobber: output stores need no ordering w.r.t. this kernel's other
+// memory accesses -- nothing in the kernel reads them back -- so shared-memory loads
+// of the next vectors may be scheduled ahead of them)
 __device__ __forceinline__ void st_vec(void* p, const uint4& v) {
     asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w)
-                 : "memory");
+                 "r"(v.z), "r"(v.w));
 }
 
 // ------------------------------------------------------------------ fast u32 division

@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
         const int64_t chw = a.C * a.HW;
         const uint32_t step = AT * V;
         const bool step_inc = hw >= step;  // at most one plane boundary per step
+        const int64_t jump = (int64_t)step + chw - hw;  // pointer step across a plane boundary
         for (uint32_t s = 0; s < nT; ++s) {
             const int64_t cp = q + s * Q;
             const uint32_t b = s % nbuf, slot = s & 1u;
@@ -447,9 +448,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
             const uint4* ds = xs + a.cap;
             const float2 P = cs[slot].P, Q2 = cs[slot].Q;
             const float mu = cs[slot].mu;
-            // output cursor: plane jn / offset jsp of this thread's current vector; within a
-            // chunk the thread visits v = c_lo + at, + AT, ... (channel-space steps of AT*V)
-            uint32_t jn = 0, jsp = 0;
+            // output cursor: pointer of this thread's current vector, plus its offset jsp in
+            // the plane; within a chunk the thread visits v = c_lo + at, + AT, ... i.e.
+            // channel-space steps of AT*V elements (one plane wrap at most when step <= HW)
+            uint32_t jsp = 0;
+            T* dst = nullptr;
             T* const outc = out + cp * a.HW;
             auto apply_vec = [&](const uint32_t v) {
                 float2 w[NP];
@@ -474,27 +477,28 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                         w[i] = fma2(al, dd[i], fma2(ka, w[i], cc2));
                     }
                 }
-                T* dst = outc + (int64_t)jn * chw + jsp;
+                T* const here = dst;
                 if (step_inc) {
                     jsp += step;
-                    if (jsp >= hw) {
-                        jsp -= hw;
-                        ++jn;
-                    }
+                    const bool wrap = jsp >= hw;
+                    jsp = wrap ? jsp - hw : jsp;
+                    dst += wrap ? jump : (int64_t)step;
                 } else {
-                    const uint32_t j = jn * hw + jsp + step;
-                    jn = fdiv(j, a.fd_hw);
-                    jsp = j - jn * hw;
+                    const uint32_t j = (uint32_t)((dst - outc) / chw) * hw + jsp + step;
+                    const uint32_t n = fdiv(j, a.fd_hw);
+                    jsp = j - n * hw;
+                    dst = outc + (int64_t)n * chw + jsp;
                 }
-                if (!(a.debug & 2u)) st_vec(dst, Pairs<T>::store(w));
+                if (!(a.debug & 2u)) st_vec(here, Pairs<T>::store(w));
             };
             for (int k = 0; k < nch; ++k) {
                 const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
                 uint32_t v = c_lo + at;
                 {
                     const uint32_t j0 = (vlo + v) * V;
-                    jn = fdiv(j0, a.fd_hw);
-                    jsp = j0 - jn * hw;
+                    const uint32_t n0 = fdiv(j0, a.fd_hw);
+                    jsp = j0 - n0 * hw;
+                    dst = outc + (int64_t)n0 * chw + jsp;
                 }
                 for (; v + 3 * AT < c_hi; v += 4 * AT) {
                     apply_vec(v);
