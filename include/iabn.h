@@ -88,6 +88,12 @@ enum {
     /* sync backward: return the all-rank sums as dgamma/dbeta (default: this rank's
        contribution, to be summed by the caller's data-parallel gradient reduction). */
     IABN_SYNC_GLOBAL_PARAM_GRADS = 1u << 3,
+    /* backward: accumulate per-element products dy*x^ (InPlace-ABN I, Alg. 2 l.5-6).
+       Default for the channel-resident schedule is the BN-dagger reduction of
+       InPlace-ABN II (Alg. 2 l.7-8): sum dy and sum dy*y, then
+       sum dy*x^ = (sum dy*y - beta sum dy)/g per channel -- the same gradient with
+       fewer operations per element. */
+    IABN_VARIANT_I = 1u << 5,
     /* forward with fixed running statistics (test time): no batch
        statistics, running stats read-only, save_* untouched. */
     IABN_EVAL = 1u << 4,

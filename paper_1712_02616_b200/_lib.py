@@ -24,6 +24,7 @@ GAMMA_FIXED_ONE = 1 << 1
 RUNNING_VAR_BIASED = 1 << 2
 SYNC_GLOBAL_PARAM_GRADS = 1 << 3
 EVAL = 1 << 4
+VARIANT_I = 1 << 5
 FORCE_STREAMING = 1 << 8
 FORCE_FUSED = 1 << 9
 

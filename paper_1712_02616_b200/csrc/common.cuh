@@ -259,6 +259,28 @@ __device__ __forceinline__ float2 bf16x2_sub_f2(uint32_t w, float k) {
         : "r"(w), "f"(k));
     return make_float2(a, b);
 }
+// Packed bf16 helpers of the backward reduction (no unpacking):
+// 1.0 in each half where the bf16 value is < 0 (-0.0 is not), else 0.0 (HSET2.BF16)
+__device__ __forceinline__ uint32_t bf16x2_ind_neg(uint32_t w) {
+    uint32_t d;
+    asm("set.lt.bf16x2.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(w), "r"(0u));
+    return d;
+}
+// acc.{x,y} += w.{lo,hi}  (FHADD.BF16: fp32 add of a bf16 operand, exact widening)
+__device__ __forceinline__ void bf16x2_acc(float2& acc, uint32_t w) {
+    asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\t"
+        "add.f32.bf16 %0, lo, %0;\n\tadd.f32.bf16 %1, hi, %1;\n}"
+        : "+f"(acc.x), "+f"(acc.y)
+        : "r"(w));
+}
+// acc.{x,y} += a.{lo,hi} * b.{lo,hi}  (FHFMA.BF16: bf16 x bf16 product, fp32 accumulate)
+__device__ __forceinline__ void bf16x2_acc_mul(float2& acc, uint32_t a, uint32_t b) {
+    asm("{\n\t.reg .b16 a0, a1, b0, b1;\n\tmov.b32 {a0, a1}, %2;\n\tmov.b32 {b0, b1}, %3;\n\t"
+        "fma.rn.f32.bf16 %0, a0, b0, %0;\n\tfma.rn.f32.bf16 %1, a1, b1, %1;\n}"
+        : "+f"(acc.x), "+f"(acc.y)
+        : "r"(a), "r"(b));
+}
+
 // fp32 pair -> bf16 pair, round to nearest even (F2FP.BF16.F32.PACK_AB).
 __device__ __forceinline__ uint32_t f2_to_bf16x2(float2 v) {
     __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);

@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                     //   alpha = g rstd, kappa = -rstd S2/m, cc = rstd (S2 beta - g S1)/m
                     // with dy, y on the branch of sign(z):
                     //   z >= 0: alpha dz + kappa z + cc;  z < 0: (alpha a) dz + (kappa / a) z + cc
+                    // variant II pushed (S1, Q = sum dy y): S2 = (Q - beta S1) / g
+                    if (!(a.flags & kVariantI)) v[1] = (v[1] - bet * v[0]) / g;
                     const double rm = rstd_b * inv_m;
                     const float alpha = (float)(g * rstd_b);
                     const float kappa = (float)(-rm * v[1]);
@@ -349,6 +351,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 ig2 = make_float2(ia.inv_g, ia.inv_g);
                 nb2 = make_float2(ia.nb, ia.nb);
             }
+            // backward variant II (BN-dagger, Alg. 2 l.7-8): per channel
+            // S1 = sum dy and Q = sum dy y = sum dz z (f' f^-1 = id on each branch), then
+            // S2 = sum dy x^ = (Q - beta S1) / g on the exchange warp.  For bf16 storage the
+            // sums run on the packed halves: S1 = sum dz - (1 - a) sum_{z<0} dz with the
+            // z < 0 indicator from HSET2, products exact in FHFMA.BF16 (no unpacking).
+            const bool v2 = !(a.flags & kVariantI);
+            float2 sn[NP];  // bf16 variant II: sum of dz over z < 0
+#pragma unroll
+            for (int i = 0; i < NP; ++i) sn[i] = make_float2(0.f, 0.f);
             auto reduce_vec = [&](const uint32_t v) {
                 if (PASS == 0) {
                     float2 d[NP];
@@ -358,10 +369,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                         s1[i] = add2(s1[i], d[i]);
                         s2[i] = fma2(d[i], d[i], s2[i]);
                     }
+                } else if (v2 && sizeof(T) == 2) {
+                    const uint4 zu = xs[v], du = ds[v];
+                    const uint32_t zw[4] = {zu.x, zu.y, zu.z, zu.w};
+                    const uint32_t dw[4] = {du.x, du.y, du.z, du.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        bf16x2_acc(s1[i], dw[i]);                        // sum dz
+                        bf16x2_acc_mul(sn[i], dw[i], bf16x2_ind_neg(zw[i]));  // sum_{z<0} dz
+                        bf16x2_acc_mul(s2[i], dw[i], zw[i]);             // sum dz z
+                    }
                 } else {
-                    // Alg. 2 l.2-5: dy = f'(z) dz; dy x^ = dy (y inv_g + nb) and dy y = dz z
-                    // (f' f^-1 is the identity on each branch), so per element
-                    // dy x^ = (dz z) inv_g + nb dy  (variant I: per-element products).
                     float2 zz[NP], dd[NP];
                     Pairs<T>::load(xs[v], zz);
                     Pairs<T>::load(ds[v], dd);
@@ -370,9 +388,13 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                         const float2 sel = make_float2(zz[i].x >= 0.f ? 1.f : a.slope,
                                                        zz[i].y >= 0.f ? 1.f : a.slope);
                         const float2 dy = mul2(dd[i], sel);
-                        const float2 p = mul2(dd[i], zz[i]);
                         s1[i] = add2(s1[i], dy);
-                        s2[i] = add2(s2[i], fma2(p, ig2, mul2(dy, nb2)));
+                        if (v2) {
+                            s2[i] = fma2(dd[i], zz[i], s2[i]);  // sum dz z
+                        } else {
+                            // variant I: per element dy x^ = (dz z) inv_g + nb dy
+                            s2[i] = add2(s2[i], fma2(mul2(dd[i], zz[i]), ig2, mul2(dy, nb2)));
+                        }
                     }
                 }
             };
@@ -390,12 +412,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 }
                 for (; v < c_hi; v += RT) reduce_vec(v);
             }
-            double d1 = 0.0, d2 = 0.0;
+            double d1 = 0.0, d2 = 0.0, dn = 0.0;
 #pragma unroll
             for (int i = 0; i < NP; ++i) {
                 d1 += (double)s1[i].x + (double)s1[i].y;
                 d2 += (double)s2[i].x + (double)s2[i].y;
+                dn += (double)sn[i].x + (double)sn[i].y;
             }
+            if (PASS == 1 && v2 && sizeof(T) == 2) d1 -= (1.0 - (double)a.slope) * dn;  // S1
             d1 = warp_sum(d1);
             d2 = warp_sum(d2);
             if (lane == 0) {

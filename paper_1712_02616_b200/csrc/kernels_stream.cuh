@@ -20,7 +20,12 @@ namespace iabn {
 constexpr int kUnroll = 4;
 
 // Gamma reparametrisation (R4).
-enum : uint32_t { kGammaPlain = 1u << 0, kGammaFixedOne = 1u << 1, kRunVarBiased = 1u << 2 };
+enum : uint32_t {
+    kGammaPlain = 1u << 0,
+    kGammaFixedOne = 1u << 1,
+    kRunVarBiased = 1u << 2,
+    kVariantI = 1u << 5  // fused backward: per-element x^ products (Alg. 2 I) instead of BN-dagger sums
+};
 
 __device__ __forceinline__ double gamma_eff(float gamma, float eps, uint32_t flags) {
     if (flags & kGammaFixedOne) return 1.0;

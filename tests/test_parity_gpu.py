@@ -243,3 +243,25 @@ def test_kernels_launch_through_the_library():
     import os
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libiabn.so" in maps
+
+
+# ------------------------------------------------------------------ backward variants (Alg. 2 I / II)
+VARIANT_I = 1 << 5
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("flags", [0, VARIANT_I], ids=["II", "I"])
+def test_backward_variants(dtype, flags):
+    _check(Case(8, 32, 784, dtype=dtype, seed=14), flags)
+
+
+@pytest.mark.parametrize("flags", [0, VARIANT_I, STREAM], ids=["II", "I", "streaming"])
+def test_large_beta_over_gamma(flags):
+    """|beta / gamma| = 20: the cancellation of the BN-dagger sum (Q - beta S1)/g
+     stays within the fp32 tolerance."""
+    case = Case(8, 16, 784, seed=15)
+    x, dz, p = inputs(case)
+    p.beta = (20.0 * p.gamma.abs()).contiguous()
+    got = run_gpu(case, x, dz, p, flags=flags)
+    ref = run_oracle(case, x, dz, p)
+    compare(case, got, ref, p)
