@@ -379,7 +379,7 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         static unsigned long long* buf = nullptr;
         static size_t cap = 0;
         const uint32_t per = (uint32_t)((a.C + p.clusters - 1) / p.clusters);
-        const size_t need = (size_t)p.clusters * p.K * per * 8;
+        const size_t need = (size_t)p.clusters * p.K * per * kTraceFields;
         if (need > cap) {
             if (buf) cudaFree(buf);
             cudaMalloc(&buf, need * sizeof(unsigned long long));

@@ -54,11 +54,11 @@ struct FusedArgs {
     FastDiv fd_hw;
     uint32_t cap;         // 16-byte vectors reserved per input per buffer (>= slice)
     uint32_t chunk_vecs;  // vectors per chunk (per input)
-    uint32_t nbuf;        // slab buffers in the ring (2..kMaxBuf)
+    uint32_t nbuf;        // slab buffers in the ring (1..kMaxBuf)
     float momentum, eps, slope, inv_slope;
     uint32_t flags;
-    uint32_t debug;  // experiments only (IABN_FUSED_DEBUG): 2 = skip the output stores,
-                     // 4 = record phase timestamps into `trace`
+    uint32_t debug;  // experiments only (IABN_FUSED_DEBUG): 4 = record phase timestamps
+                     // into `trace`
     unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
     uint32_t trace_ch;          // channels per CTA recorded
 };
@@ -70,11 +70,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 // phase timestamps (debug & 4): 0 producer issued chunk 0, 1 producer issued last chunk,
 // 2 reduce got chunk 0, 3 reduce got last chunk, 4 record pushed, 5 exchange gathered,
-// 6 apply start, 7 apply end
-#define IABN_TRACE(a, t, slot)                                                          \
-    do {                                                                                \
-        if (((a).debug & 4u) && (t) < (a).trace_ch)                                    \
-            (a).trace[((size_t)blockIdx.x * (a).trace_ch + (t)) * 8 + (slot)] = gtimer(); \
+// 6 apply start, 7 apply end, 8 reduce loop done (thread 0), 9 group partials summed,
+// 10 own record slots free (before the push), 11 coefficients published
+constexpr int kTraceFields = 12;
+#define IABN_TRACE(a, t, slot)                                                              \
+    do {                                                                                    \
+        if (((a).debug & 4u) && (t) < (a).trace_ch)                                        \
+            (a).trace[((size_t)blockIdx.x * (a).trace_ch + (t)) * kTraceFields + (slot)] =  \
+                gtimer();                                                                   \
     } while (0)
 
 __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
@@ -148,21 +151,16 @@ constexpr int kFusedThreads = (kProducerWarp + 1) * 32;
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
-__device__ __forceinline__ void reducer_sync() {  // named barrier over the reduce warps
-    asm volatile("bar.sync 1, %0;" ::"n"(kReduceWarps * 32) : "memory");
+// named barrier over a worker group (id 1: reduce warps, 2: apply warps)
+__device__ __forceinline__ void group_sync(uint32_t id, uint32_t nthr) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
 }
-__device__ __forceinline__ void applier_sync() {  // named barrier over the apply warps
-    asm volatile("bar.sync 2, %0;" ::"n"(kApplyWarps * 32) : "memory");
-}
-// One warp of a group polls the mbarrier; the rest block on a named barrier (no
-// issue slots burnt by a whole group of waiting warps).
-template <int GROUP>
-__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool leader) {
+// One warp of a group polls the mbarrier; the rest block on the group's named
+// barrier (no issue slots burnt by a whole group of waiting warps).
+__device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool leader, uint32_t id,
+                                           uint32_t nthr) {
     if (leader) mbar_wait(bar, parity);
-    if (GROUP == 1)
-        reducer_sync();
-    else
-        applier_sync();
+    group_sync(id, nthr);
 }
 
 template <typename T, int PASS>
@@ -179,7 +177,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
     __shared__ __align__(8) uint64_t ready[2];                   // exchange -> apply warps
     __shared__ __align__(8) uint64_t freed[2];                   // apply warps -> exchange
     __shared__ __align__(16) double rec[kSlots][kMaxCluster][4];  // pushed by the K peers
-    __shared__ double red[2][2][kReduceWarps];
+    __shared__ double red[2][2][kReduceWarps + kApplyWarps];
     __shared__ ApplyCoef cs[2];
 
     const uint32_t K = cluster_nctarank(), r = cluster_ctarank();
@@ -192,13 +190,18 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
     const uint32_t nv = vhi - vlo;
     const int nch = (int)((nv + a.chunk_vecs - 1) / a.chunk_vecs);
     const size_t bufv = (size_t)NIN * a.cap;  // vectors per slab buffer
+    const uint32_t smem_u32 = smem_addr(smem);
+    const uint32_t pv = (uint32_t)a.HW / V;  // vectors per plane
+    // whole-plane slices and chunks (the usual case): plane-structured output addressing
+    const bool plane_chunks = vlo % pv == 0 && a.chunk_vecs % pv == 0;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t apply_warps = kApplyWarps;
 
     if (threadIdx.x == 0) {
         for (uint32_t b = 0; b < nbuf; ++b) {
             for (int k = 0; k < nch; ++k) {
                 mbar_init(&full[b][k], 1);
-                mbar_init(&empty[b][k], kApplyWarps);
+                mbar_init(&empty[b][k], apply_warps);
             }
         }
         for (int i = 0; i < kSlots; ++i) {
@@ -207,7 +210,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&ready[i], 1);
-            mbar_init(&freed[i], kApplyWarps);
+            mbar_init(&freed[i], apply_warps);
         }
         fence_mbar_init();
     }
@@ -264,14 +267,17 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
             if (s >= 2) mbar_wait(&freed[slot], (s / 2 - 1) & 1u);
             constexpr uint32_t RB = NR == 3 ? 32u : 16u;  // record bytes per peer
             // per-channel terms that do not depend on the records, before the wait
-            double g = 0.0, bet = 0.0, rstd_b = 0.0;
+            double g = 0.0, bet = 0.0, rstd_b = 0.0, inv_g = 0.0;
             if (lane == 0) {
                 g = gamma_eff(a.gamma[cp], a.eps, a.flags);
+                inv_g = PASS == 1 ? 1.0 / g : 0.0;
                 bet = (double)a.beta[cp];
                 if (PASS == 1) rstd_b = rsqrt((double)a.save_var[cp] + (double)a.eps);
                 mbar_arrive_expect_tx(&gathered[rs], K * RB);
             }
-            mbar_wait_cluster(&gathered[rs], (s / kSlots) & 1u);
+            // the records are st.async transactions on my own barrier: completing the phase
+            // makes them visible, as for a TMA load (CTA-scope acquire, no L1 invalidation)
+            mbar_wait(&gathered[rs], (s / kSlots) & 1u);
             if (lane == 0) IABN_TRACE(a, s, 5);
             // fold: lane j < K takes rank j's record, then a fixed xor tree (the same
             // order in every CTA of the cluster => bit-identical coefficients)
@@ -296,6 +302,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                     cs[slot].Q = make_float2(Bp, Bp);
                     cs[slot].mu = mu_hi;
                     mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
+                    IABN_TRACE(a, s, 11);
                     if (r == 0) {
                         a.save_mean[cp] = (float)mean;
                         a.save_var[cp] = (float)var;
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                     // with dy, y on the branch of sign(z):
                     //   z >= 0: alpha dz + kappa z + cc;  z < 0: (alpha a) dz + (kappa / a) z + cc
                     // variant II pushed (S1, Q = sum dy y): S2 = (Q - beta S1) / g
-                    if (!(a.flags & kVariantI)) v[1] = (v[1] - bet * v[0]) / g;
+                    if (!(a.flags & kVariantI)) v[1] = (v[1] - bet * v[0]) * inv_g;
                     const double rm = rstd_b * inv_m;
                     const float alpha = (float)(g * rstd_b);
                     const float kappa = (float)(-rm * v[1]);
@@ -317,6 +324,7 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                     cs[slot].Q = make_float2(alpha * a.slope, kappa * a.inv_slope);
                     cs[slot].mu = cc;
                     mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
+                    IABN_TRACE(a, s, 11);
                     if (r == 0) {
                         a.dbeta[cp] = (float)v[0];
                         a.dgamma[cp] = (float)(gamma_sign(a.gamma[cp], a.flags) * v[1]);
@@ -327,24 +335,28 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
             // the slot of every peer that pushed into me may be reused by it
             if (lane < K) mbar_arrive_cluster(mapa(&slotfree[rs], lane));
         }
-    } else if (warp < kReduceWarps) {
-        // ================================================ reduce warps: channel sums over the
-        // resident slice; the CTA record is pushed into all K peers (DSMEM)
-        constexpr int RT = kReduceWarps * 32;
-        for (uint32_t t = 0; t < nT; ++t) {
+    }
+
+    // ==================================================== reduce (slice t): channel sums over
+    // the resident slice; the CTA record is pushed into all K peers (DSMEM).  Threads
+    // tid < RT of a group with named barrier gb; warp tid / 32 == 0 folds and pushes.
+    auto reduce_slice = [&](const uint32_t t, const uint32_t tid, const uint32_t RT,
+                            const uint32_t gb) {
+        const uint32_t gw = tid >> 5;
+        {
             const int64_t c = q + t * Q;
             const uint32_t b = t % nbuf, par = (t / nbuf) & 1u;
-            const uint4* xs = smem + b * bufv;  // x (fwd) or z (bwd)
-            const uint4* ds = xs + a.cap;       // dz (bwd)
+            const uint32_t xs = smem_u32 + (uint32_t)(b * bufv * 16);  // x (fwd) or z (bwd)
+            const uint32_t ds = xs + a.cap * 16u;                      // dz (bwd)
             float2 s1[NP], s2[NP];
 #pragma unroll
             for (int i = 0; i < NP; ++i) s1[i] = s2[i] = make_float2(0.f, 0.f);
             float K0 = 0.f;
             float2 ig2 = make_float2(0.f, 0.f), nb2 = ig2;
             if (PASS == 0) {
-                group_wait<1>(&full[b][0], par, warp == 0);
+                group_wait(&full[b][0], par, gw == 0, gb, RT);
                 float2 p0[NP];
-                Pairs<T>::load(xs[0], p0);
+                Pairs<T>::load(lds128(xs), p0);
                 K0 = p0[0].x;  // shift: a sample of this slice (cancellation-free variance)
             } else {
                 const InvAffine ia = inv_affine(__ldg(a.gamma + c), __ldg(a.beta + c), a.eps, a.flags);
@@ -363,14 +375,14 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
             auto reduce_vec = [&](const uint32_t v) {
                 if (PASS == 0) {
                     float2 d[NP];
-                    Pairs<T>::load_sub(xs[v], K0, d);
+                    Pairs<T>::load_sub(lds128(xs + v * 16u), K0, d);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
                         s1[i] = add2(s1[i], d[i]);
                         s2[i] = fma2(d[i], d[i], s2[i]);
                     }
                 } else if (v2 && sizeof(T) == 2) {
-                    const uint4 zu = xs[v], du = ds[v];
+                    const uint4 zu = lds128(xs + v * 16u), du = lds128(ds + v * 16u);
                     const uint32_t zw[4] = {zu.x, zu.y, zu.z, zu.w};
                     const uint32_t dw[4] = {du.x, du.y, du.z, du.w};
 #pragma unroll
@@ -381,8 +393,8 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                     }
                 } else {
                     float2 zz[NP], dd[NP];
-                    Pairs<T>::load(xs[v], zz);
-                    Pairs<T>::load(ds[v], dd);
+                    Pairs<T>::load(lds128(xs + v * 16u), zz);
+                    Pairs<T>::load(lds128(ds + v * 16u), dd);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) {
                         const float2 sel = make_float2(zz[i].x >= 0.f ? 1.f : a.slope,
@@ -399,11 +411,11 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 }
             };
             for (int k = 0; k < nch; ++k) {
-                if (PASS == 1 || k > 0) group_wait<1>(&full[b][k], par, warp == 0);
-                if (threadIdx.x == 0 && k == 0) IABN_TRACE(a, t, 2);
-                if (threadIdx.x == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
+                if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
+                if (tid == 0 && k == 0) IABN_TRACE(a, t, 2);
+                if (tid == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
                 const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-                uint32_t v = c_lo + threadIdx.x;
+                uint32_t v = c_lo + tid;
                 for (; v + 3 * RT < c_hi; v += 4 * RT) {
                     reduce_vec(v);
                     reduce_vec(v + RT);
@@ -412,24 +424,34 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 }
                 for (; v < c_hi; v += RT) reduce_vec(v);
             }
-            double d1 = 0.0, d2 = 0.0, dn = 0.0;
+            if (tid == 0) IABN_TRACE(a, t, 8);
+            // fold the thread's fp32 chains and the warp in fp32 (a few rounding steps on
+            // partial sums of at most a few thousand terms), the warps and CTAs in fp64
 #pragma unroll
-            for (int i = 0; i < NP; ++i) {
-                d1 += (double)s1[i].x + (double)s1[i].y;
-                d2 += (double)s2[i].x + (double)s2[i].y;
-                dn += (double)sn[i].x + (double)sn[i].y;
+            for (int h = NP / 2; h > 0; h >>= 1)
+#pragma unroll
+                for (int i = 0; i < h; ++i) {
+                    s1[i] = add2(s1[i], s1[i + h]);
+                    s2[i] = add2(s2[i], s2[i + h]);
+                    sn[i] = add2(sn[i], sn[i + h]);
+                }
+            float f1 = s1[0].x + s1[0].y, f2 = s2[0].x + s2[0].y;
+            if (PASS == 1 && v2 && sizeof(T) == 2) f1 -= (1.f - a.slope) * (sn[0].x + sn[0].y);  // S1
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                f1 += __shfl_xor_sync(0xffffffffu, f1, o);
+                f2 += __shfl_xor_sync(0xffffffffu, f2, o);
             }
-            if (PASS == 1 && v2 && sizeof(T) == 2) d1 -= (1.0 - (double)a.slope) * dn;  // S1
-            d1 = warp_sum(d1);
-            d2 = warp_sum(d2);
+            const double d1 = f1, d2 = f2;
             if (lane == 0) {
-                red[t & 1][0][warp] = d1;
-                red[t & 1][1][warp] = d2;
+                red[t & 1][0][gw] = d1;
+                red[t & 1][1][gw] = d2;
             }
-            reducer_sync();
-            if (warp == 0) {
+            group_sync(gb, RT);
+            if (gw == 0) {
+                if (tid == 0) IABN_TRACE(a, t, 9);
                 double S1 = 0.0, S2 = 0.0;
-                for (int w = 0; w < kReduceWarps; ++w) {
+                for (uint32_t w = 0; w < RT / 32; ++w) {
                     S1 += red[t & 1][0][w];
                     S2 += red[t & 1][1][w];
                 }
@@ -442,7 +464,9 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 }
                 const uint32_t rs = t % kSlots;
                 // my record slot rs in every peer must have been folded (channel t - kSlots)
-                if (t >= (uint32_t)kSlots) mbar_wait_cluster(&slotfree[rs], (t / kSlots - 1) & 1u);
+                // (write-after-read only: the peers' release-arrivals follow their reads)
+                if (t >= (uint32_t)kSlots) mbar_wait(&slotfree[rs], (t / kSlots - 1) & 1u);
+                if (lane == 0) IABN_TRACE(a, t, 10);
                 if (lane < K) {  // lane j pushes this CTA's record into peer j (st.async)
                     const uint32_t mb = mapa(&gathered[rs], lane);
                     st_async_f64x2(mapa(&rec[rs][r][0], lane), out[0], out[1], mb);
@@ -451,92 +475,116 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 if (lane == 0) IABN_TRACE(a, t, 4);
             }
         }
-    } else {
-        // ================================================ apply warps: outputs from the resident
-        // slice once the channel's coefficients are in (the reduce warps have read it by then)
+    };
+
+    // ==================================================== apply (slice s): outputs from the
+    // resident slice once the channel's coefficients are in (the reduce has read it by then).
+    // Threads at < AT of a group with named barrier gb; warp 0 of the group polls.
+    auto apply_slice = [&](const uint32_t s, const uint32_t at, const uint32_t AT,
+                           const uint32_t gb) {
         const uint32_t hw = (uint32_t)a.HW;
         const float2 sl2 = make_float2(a.slope, a.slope);
-        constexpr int AT = kApplyWarps * 32;
-        const uint32_t at = threadIdx.x - kReduceWarps * 32;
         T* out = (T*)a.out;
         const int64_t chw = a.C * a.HW;
-        const uint32_t step = AT * V;
-        const bool step_inc = hw >= step;  // at most one plane boundary per step
-        const int64_t jump = (int64_t)step + chw - hw;  // pointer step across a plane boundary
-        for (uint32_t s = 0; s < nT; ++s) {
-            const int64_t cp = q + s * Q;
-            const uint32_t b = s % nbuf, slot = s & 1u;
-            group_wait<2>(&ready[slot], (s / 2) & 1u, warp == kReduceWarps);
-            if (at == 0) IABN_TRACE(a, s, 6);
-            const uint4* xs = smem + b * bufv;
-            const uint4* ds = xs + a.cap;
-            const float2 P = cs[slot].P, Q2 = cs[slot].Q;
-            const float mu = cs[slot].mu;
-            // output cursor: pointer of this thread's current vector, plus its offset jsp in
-            // the plane; within a chunk the thread visits v = c_lo + at, + AT, ... i.e.
-            // channel-space steps of AT*V elements (one plane wrap at most when step <= HW)
-            uint32_t jsp = 0;
-            T* dst = nullptr;
-            T* const outc = out + cp * a.HW;
-            auto apply_vec = [&](const uint32_t v) {
-                float2 w[NP];
-                if (PASS == 0) {
-                    Pairs<T>::load_sub(xs[v], mu, w);
+        const int64_t cp = q + s * Q;
+        const uint32_t b = s % nbuf, slot = s & 1u;
+        group_wait(&ready[slot], (s / 2) & 1u, at < 32, gb, AT);
+        if (at == 0) IABN_TRACE(a, s, 6);
+        const uint32_t xs = smem_u32 + (uint32_t)(b * bufv * 16);  // shared address of x / z
+        const uint32_t ds = xs + a.cap * 16u;                      // dz (bwd)
+        const float2 P = cs[slot].P, Q2 = cs[slot].Q;
+        const float mu = cs[slot].mu;
+        T* const outc = out + cp * a.HW;
+        // whole-plane chunks with planes of at least AT vectors: per-plane addressing
+        const bool plane_loop = plane_chunks && pv >= AT;
+        // outputs of the slice's vector v (shared memory) into dst (global)
+        auto apply_vec = [&](const uint32_t v, T* const dst) {
+            float2 w[NP];
+            if (PASS == 0) {
+                Pairs<T>::load_sub(lds128(xs + v * 16u), mu, w);
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) {
-                        const float2 y = fma2(w[i], P, Q2);
-                        const float2 ay = mul2(y, sl2);  // f(y) = max(y, a y) for 0 < a <= 1
-                        w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
-                    }
-                } else {
-                    float2 dd[NP];
-                    Pairs<T>::load(xs[v], w);
-                    Pairs<T>::load(ds[v], dd);
-                    const float2 cc2 = make_float2(mu, mu);
+                for (int i = 0; i < NP; ++i) {
+                    const float2 y = fma2(w[i], P, Q2);
+                    const float2 ay = mul2(y, sl2);  // f(y) = max(y, a y) for 0 < a <= 1
+                    w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                }
+            } else {
+                float2 dd[NP];
+                Pairs<T>::load(lds128(xs + v * 16u), w);
+                Pairs<T>::load(lds128(ds + v * 16u), dd);
+                const float2 cc2 = make_float2(mu, mu);
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) {
-                        const bool px = w[i].x >= 0.f, py = w[i].y >= 0.f;
-                        const float2 al = make_float2(px ? P.x : Q2.x, py ? P.x : Q2.x);
-                        const float2 ka = make_float2(px ? P.y : Q2.y, py ? P.y : Q2.y);
-                        w[i] = fma2(al, dd[i], fma2(ka, w[i], cc2));
-                    }
+                for (int i = 0; i < NP; ++i) {
+                    const bool px = w[i].x >= 0.f, py = w[i].y >= 0.f;
+                    const float2 al = make_float2(px ? P.x : Q2.x, py ? P.x : Q2.x);
+                    const float2 ka = make_float2(px ? P.y : Q2.y, py ? P.y : Q2.y);
+                    w[i] = fma2(al, dd[i], fma2(ka, w[i], cc2));
                 }
-                T* const here = dst;
-                if (step_inc) {
-                    jsp += step;
-                    const bool wrap = jsp >= hw;
-                    jsp = wrap ? jsp - hw : jsp;
-                    dst += wrap ? jump : (int64_t)step;
-                } else {
-                    const uint32_t j = (uint32_t)((dst - outc) / chw) * hw + jsp + step;
-                    const uint32_t n = fdiv(j, a.fd_hw);
-                    jsp = j - n * hw;
-                    dst = outc + (int64_t)n * chw + jsp;
-                }
-                if (!(a.debug & 2u)) st_vec(here, Pairs<T>::store(w));
-            };
-            for (int k = 0; k < nch; ++k) {
-                const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-                uint32_t v = c_lo + at;
-                {
-                    const uint32_t j0 = (vlo + v) * V;
-                    const uint32_t n0 = fdiv(j0, a.fd_hw);
-                    jsp = j0 - n0 * hw;
-                    dst = outc + (int64_t)n0 * chw + jsp;
-                }
-                for (; v + 3 * AT < c_hi; v += 4 * AT) {
-                    apply_vec(v);
-                    apply_vec(v + AT);
-                    apply_vec(v + 2 * AT);
-                    apply_vec(v + 3 * AT);
-                }
-                for (; v < c_hi; v += AT) apply_vec(v);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[b][k]);  // chunk k of buffer b may be refilled
             }
-            if (at == 0) IABN_TRACE(a, s, 7);
-            if (lane == 0) mbar_arrive(&freed[slot]);  // coefficient slot may be rewritten
+            st_vec(dst, Pairs<T>::store(w));
+        };
+        for (int k = 0; k < nch; ++k) {
+            const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+            if (plane_loop) {
+                // the chunk is whole planes: plane n of the channel is vectors [pb, pb + pv).
+                // Thread `at` takes the chunk's vectors u = at, at + AT, ... (u = pb - c_lo + v),
+                // i.e. in each plane the v with v = at - off (mod AT), off = (pb - c_lo) % AT
+                uint32_t n = (vlo + c_lo) / pv, off = 0;
+                const uint32_t pv_mod = pv % AT;
+                for (uint32_t pb = c_lo; pb < c_hi; pb += pv, ++n) {
+                    T* const dp = outc + (int64_t)n * chw;
+                    uint32_t v = at >= off ? at - off : at + AT - off;
+                    for (; v + 3 * AT < pv; v += 4 * AT) {
+                        apply_vec(pb + v, dp + v * V);
+                        apply_vec(pb + v + AT, dp + (v + AT) * V);
+                        apply_vec(pb + v + 2 * AT, dp + (v + 2 * AT) * V);
+                        apply_vec(pb + v + 3 * AT, dp + (v + 3 * AT) * V);
+                    }
+                    for (; v < pv; v += AT) apply_vec(pb + v, dp + v * V);
+                    off += pv_mod;
+                    off = off >= AT ? off - AT : off;
+                }
+            } else {
+                // output cursor: the thread visits v = c_lo + at, + AT, ... i.e. channel-space
+                // steps of AT*V elements: one plane wrap at most when the step <= HW, else
+                // the plane by division
+                const uint32_t step = AT * V;
+                const int64_t jump = (int64_t)step + chw - hw;  // step across a plane boundary
+                uint32_t v = c_lo + at;
+                const uint32_t j0 = (vlo + v) * V;
+                const uint32_t n0 = fdiv(j0, a.fd_hw);
+                uint32_t jsp = j0 - n0 * hw;
+                T* dst = outc + (int64_t)n0 * chw + jsp;
+                if (hw >= step) {
+                    for (; v < c_hi; v += AT) {
+                        apply_vec(v, dst);
+                        jsp += step;
+                        const bool wrap = jsp >= hw;
+                        jsp = wrap ? jsp - hw : jsp;
+                        dst += wrap ? jump : (int64_t)step;
+                    }
+                } else {
+                    for (; v < c_hi; v += AT) {
+                        const uint32_t j = (vlo + v) * V;
+                        const uint32_t n = fdiv(j, a.fd_hw);
+                        apply_vec(v, outc + (int64_t)n * chw + (j - n * hw));
+                    }
+                }
+            }
+            __syncwarp();
+            if ((at & 31) == 0) mbar_arrive(&empty[b][k]);  // chunk k of buffer b may be refilled
         }
+        if (at == 0) IABN_TRACE(a, s, 7);
+        if ((at & 31) == 0) mbar_arrive(&freed[slot]);  // coefficient slot may be rewritten
+    };
+
+    if (warp >= (uint32_t)kExchangeWarp) {
+        // producer and exchange warps: above
+    } else if (warp < kReduceWarps) {
+        for (uint32_t t = 0; t < nT; ++t) reduce_slice(t, threadIdx.x, kReduceWarps * 32, 1);
+    } else {
+        for (uint32_t s = 0; s < nT; ++s)
+            apply_slice(s, threadIdx.x - kReduceWarps * 32, kApplyWarps * 32, 2);
     }
     // peers may still push records / arrive on this CTA's barriers until they finish
     cluster_arrive_release();

@@ -17,7 +17,9 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-NAMES = ["issue0", "issueN", "got0", "gotN", "pushed", "gathered", "apply0", "applyN"]
+NAMES = ["issue0", "issueN", "got0", "gotN", "pushed", "gathered", "apply0", "applyN",
+         "reduced", "summed", "slotfree", "published"]
+F = len(NAMES)
 
 
 def dump(L):
@@ -25,11 +27,11 @@ def dump(L):
     buf = (ctypes.c_ulonglong * n)()
     L.lib.iabn_debug_trace(buf, n)
     per = L.lib.iabn_debug_trace_channels()
-    return np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8).astype(np.int64), per
+    return np.frombuffer(buf, dtype=np.uint64).reshape(-1, F).astype(np.int64), per
 
 
 def report(tr, label, grid_ch):
-    tr = tr.reshape(-1, grid_ch, 8)  # [cta][t][8]
+    tr = tr.reshape(-1, grid_ch, F)  # [cta][t][8]
     valid = (tr > 0).all(axis=2)
     t0 = tr[tr > 0].min()
     print(f"== {label}: {tr.shape[0]} CTAs x {grid_ch} channels, span "
@@ -38,8 +40,14 @@ def report(tr, label, grid_ch):
         "load lat (issue0->got0)": tr[..., 2] - tr[..., 0],
         "slice arrival (got0->gotN)": tr[..., 3] - tr[..., 2],
         "reduce tail (gotN->pushed)": tr[..., 4] - tr[..., 3],
+        "  last chunk (gotN->reduced)": tr[..., 8] - tr[..., 3],
+        "  fold (reduced->summed)": tr[..., 9] - tr[..., 8],
+        "  slot wait (summed->slotfree)": tr[..., 10] - tr[..., 9],
+        "  push (slotfree->pushed)": tr[..., 4] - tr[..., 10],
         "exchange (pushed->gathered)": tr[..., 5] - tr[..., 4],
         "to apply (gathered->apply0)": tr[..., 6] - tr[..., 5],
+        "  coefs (gathered->published)": tr[..., 11] - tr[..., 5],
+        "  wake (published->apply0)": tr[..., 6] - tr[..., 11],
         "apply (apply0->applyN)": tr[..., 7] - tr[..., 6],
         "residence (issue0->applyN)": tr[..., 7] - tr[..., 0],
     }
