@@ -139,10 +139,19 @@ struct ApplyCoef {
 };
 
 #ifndef IABN_REDUCE_WARPS
-#define IABN_REDUCE_WARPS 4
+#define IABN_REDUCE_WARPS 3
 #endif
 #ifndef IABN_APPLY_WARPS
-#define IABN_APPLY_WARPS 8
+#define IABN_APPLY_WARPS 4
+#endif
+#ifndef IABN_RED_UNROLL
+#define IABN_RED_UNROLL 8  // vectors per reduce-loop iteration (shared loads issued first)
+#endif
+#ifndef IABN_APP_UNROLL
+#define IABN_APP_UNROLL 4  // vectors per apply-loop iteration
+#endif
+#ifndef IABN_MIN_BLOCKS
+#define IABN_MIN_BLOCKS 2  // CTAs per SM the register allocation must allow
 #endif
 constexpr int kReduceWarps = IABN_REDUCE_WARPS;  // stream each resident slice for the channel sums
 constexpr int kApplyWarps = IABN_APPLY_WARPS;    // stream it again, one channel behind, for outputs
@@ -154,6 +163,7 @@ constexpr int kApplyWarps = IABN_APPLY_WARPS;    // stream it again, one channel
 #define IABN_WARP_ORDER 1
 #endif
 constexpr int kWorkerWarps = kReduceWarps + kApplyWarps;
+constexpr int kRU = IABN_RED_UNROLL, kAU = IABN_APP_UNROLL;
 constexpr int kProducerWarp = IABN_WARP_ORDER ? 0 : kWorkerWarps + 1;  // TMA bulk copies
 constexpr int kExchangeWarp = IABN_WARP_ORDER ? 1 : kWorkerWarps;      // folds the records
 constexpr int kApplyWarp0 = IABN_WARP_ORDER ? 2 : kReduceWarps;
@@ -176,7 +186,7 @@ __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool 
 }
 
 template <typename T, int PASS>
-__global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs a) {
+__global__ void __launch_bounds__(kFusedThreads, IABN_MIN_BLOCKS) fused_kernel(const FusedArgs a) {
     constexpr int NIN = PASS == 0 ? 1 : 2;
     constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
     constexpr int V = Elem<T>::kVec;
@@ -431,15 +441,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                     if (tid == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
                     const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
                     uint32_t v = c_lo + tid;
-                    for (; v + 3 * RT < c_hi; v += 4 * RT) {
-                        uint4 zu[4], du[4];
+                    for (; v + (kRU - 1) * RT < c_hi; v += kRU * RT) {
+                        uint4 zu[kRU], du[kRU];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < kRU; ++j) {
                             zu[j] = lds128(xs + (v + j * RT) * 16u);
                             du[j] = PASS == 1 ? lds128(ds + (v + j * RT) * 16u) : zu[j];
                         }
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) reduce_vec(zu[j], du[j], v2tag);
+                        for (int j = 0; j < kRU; ++j) reduce_vec(zu[j], du[j], v2tag);
                     }
                     for (; v < c_hi; v += RT) {
                         const uint4 zu = lds128(xs + v * 16u);
@@ -565,15 +575,15 @@ __global__ void __launch_bounds__(kFusedThreads, 2) fused_kernel(const FusedArgs
                 for (uint32_t pb = c_lo; pb < c_hi; pb += pv, ++n) {
                     T* const dp = outc + (int64_t)n * chw;
                     uint32_t v = at >= off ? at - off : at + AT - off;
-                    for (; v + 3 * AT < pv; v += 4 * AT) {  // shared loads first
-                        uint4 xu[4], du[4];
+                    for (; v + (kAU - 1) * AT < pv; v += kAU * AT) {  // shared loads first
+                        uint4 xu[kAU], du[kAU];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < kAU; ++j) {
                             xu[j] = lds128(xs + (pb + v + j * AT) * 16u);
                             du[j] = PASS == 1 ? lds128(ds + (pb + v + j * AT) * 16u) : xu[j];
                         }
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) apply_vals(xu[j], du[j], dp + (v + j * AT) * V);
+                        for (int j = 0; j < kAU; ++j) apply_vals(xu[j], du[j], dp + (v + j * AT) * V);
                     }
                     for (; v < pv; v += AT) apply_vec(pb + v, dp + v * V);
                     off += pv_mod;

@@ -1,0 +1,7 @@
+# default 3 reduce + 4 apply warps, reduce unroll 8
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo rc=$? >> gpurun_out/gpu_tests.log
+B="python bench.py --steps 60 --warmup 5 --e2e-steps 0 --no-cpu-baseline"
+timeout 300 $B > gpurun_out/e41.log 2>&1
+timeout 300 $B --config r50s3 > gpurun_out/e41_r50.log 2>&1
+IABN_FUSED_DEBUG=4 timeout 300 python tools/trace_fused.py > gpurun_out/t41.log 2>&1
+echo done
