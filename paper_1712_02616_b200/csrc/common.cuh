@@ -94,6 +94,15 @@ __device__ __forceinline__ uint4 ld_vec(const void* p) {
                  : "l"(p));
     return r;
 }
+// Same load, not volatile: the compiler may batch and hoist it (inputs that no thread
+// of the kernel writes).
+__device__ __forceinline__ uint4 ld_vec_ro(const void* p) {
+    uint4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+        : "l"(p));
+    return r;
+}
 // (no "memory" clobber: output stores need no ordering w.r.t. this kernel's other
 // memory accesses -- nothing in the kernel reads them back -- so shared-memory loads
 // of the next vectors may be scheduled ahead of them)

@@ -135,7 +135,10 @@ bool vec_ok(const Geom& g) {
 
 // Split count of the streaming reductions: independent of the device so that
 // workspace sizes and reduction trees (hence results) are fixed per shape.
-constexpr int64_t kTargetCtas = 148 * 8;
+#ifndef IABN_TARGET_WAVES
+#define IABN_TARGET_WAVES 1
+#endif
+constexpr int64_t kTargetCtas = 148 * 8 * IABN_TARGET_WAVES;
 int stat_splits(const Geom& g) {
     const int64_t target = kTargetCtas;
     int64_t units, per_unit_min, work;
@@ -503,7 +506,10 @@ iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4
         const T* xp = (const T*)x + off;
         T* zp = (T*)z + off;
         const int grid = apply_grid(E, g.b, sms);
-        if (g.layout == IABN_NCHW) {
+        if (g.layout == IABN_NCHW && al) {
+            fwd_apply_rows_kernel<T><<<grid, kThreads, 0, st>>>(
+                xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)g.HW, (uint32_t)g.C, fh, fc, slope);
+        } else if (g.layout == IABN_NCHW) {
             if (al)
                 fwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
             else

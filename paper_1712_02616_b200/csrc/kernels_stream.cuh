@@ -17,7 +17,14 @@
 
 namespace iabn {
 
-constexpr int kUnroll = 4;
+#ifndef IABN_STREAM_UNROLL
+#define IABN_STREAM_UNROLL 4
+#endif
+constexpr int kUnroll = IABN_STREAM_UNROLL;  // independent 16-byte loads in flight per thread
+#ifndef IABN_STAT_UNROLL
+#define IABN_STAT_UNROLL 8
+#endif
+constexpr int kStatUnroll = IABN_STAT_UNROLL;  // statistics kernel (one input)
 
 // Gamma reparametrisation (R4).
 enum : uint32_t {
@@ -47,6 +54,32 @@ __device__ __forceinline__ void write_raw_moments(double* out, double n, double 
     out[2] = S2 + 2.0 * K * S1 + n * K * K;
 }
 
+// Offset (from the channel's first element) of channel-space element j = v*V of an
+// NCHW channel, stepped by `step` elements at a time: at most one plane boundary per
+// step when step <= HW (pointer arithmetic only), else by division.
+struct PlaneCursor {
+    int64_t off;
+    uint32_t sp;  // offset within the plane
+    __device__ __forceinline__ void seek(uint32_t j, const FastDiv& fd_hw, uint32_t HW,
+                                         int64_t CHW) {
+        const uint32_t n = fdiv(j, fd_hw);
+        sp = j - n * HW;
+        off = (int64_t)n * CHW + sp;
+    }
+    // advance by `step` elements to channel-space element j_next
+    __device__ __forceinline__ void next(uint32_t step, uint32_t j_next, const FastDiv& fd_hw,
+                                         uint32_t HW, int64_t CHW) {
+        if (step <= HW) {
+            sp += step;
+            const bool wrap = sp >= HW;
+            sp = wrap ? sp - HW : sp;
+            off += wrap ? (int64_t)step + CHW - HW : (int64_t)step;
+        } else {
+            seek(j_next, fd_hw, HW, CHW);
+        }
+    }
+};
+
 // NCHW: grid (C, S); CTA (c, s) reduces channel-space [lo, hi) of m = N*HW values;
 // channel-space index j lives at x[((j / HW) * C + c) * HW + j % HW].
 template <typename T, bool VEC>
@@ -66,47 +99,103 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
     double d1 = 0.0, d2 = 0.0;
     int iter = 0;
-    for (uint32_t base = vlo + threadIdx.x; base < vhi; base += kThreads * kUnroll) {
-        float f[kUnroll][V];
+    if constexpr (VEC) {
+        // raw 16-byte loads first (kStatUnroll in flight per thread), unpacked and
+        // shifted by K in the math loop (bf16: FHADD.BF16), fp32x2 chains
+        constexpr int NP = Pairs<T>::kN;
+        float2 s1[NP], s2[NP];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint32_t v = base + u * kThreads;
-            if (v < vhi) {
-                const uint32_t j = v * V;
-                const uint32_t n = fdiv(j, fd_hw);
-                const T* p = xc + ((int64_t)n * C) * HW + (j - n * (uint32_t)HW);
-                if constexpr (VEC) {
-                    unpack<T>(ld_vec(p), f[u]);
+        for (int i = 0; i < NP; ++i) s1[i] = s2[i] = make_float2(0.f, 0.f);
+        auto accumulate = [&](const uint4 rv) {
+            float2 d[NP];
+            Pairs<T>::load_sub(rv, K, d);
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                s1[i] = add2(s1[i], d[i]);
+                s2[i] = fma2(d[i], d[i], s2[i]);
+            }
+        };
+        auto flush = [&]() {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                d1 += (double)s1[i].x + (double)s1[i].y;
+                d2 += (double)s2[i].x + (double)s2[i].y;
+                s1[i] = s2[i] = make_float2(0.f, 0.f);
+            }
+        };
+        const int64_t CHW = C * HW;
+        const uint32_t step = kThreads * V;
+        uint32_t v = vlo + threadIdx.x;
+        PlaneCursor cur;
+        cur.seek(v * V, fd_hw, (uint32_t)HW, CHW);
+        for (; v + (kStatUnroll - 1) * kThreads < vhi;) {
+            uint4 r[kStatUnroll];  // all in range: unpredicated loads, issued together
+#pragma unroll
+            for (int u = 0; u < kStatUnroll; ++u) {
+                r[u] = ld_vec_ro(xc + cur.off);
+                v += kThreads;
+                cur.next(step, v * V, fd_hw, (uint32_t)HW, CHW);
+            }
+#pragma unroll
+            for (int u = 0; u < kStatUnroll; ++u) accumulate(r[u]);
+            if (++iter == 8) {
+                iter = 0;
+                flush();
+            }
+        }
+        for (; v < vhi;) {
+            accumulate(ld_vec_ro(xc + cur.off));
+            v += kThreads;
+            cur.next(step, v * V, fd_hw, (uint32_t)HW, CHW);
+        }
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            d1 += (double)s1[i].x + (double)s1[i].y;
+            d2 += (double)s2[i].x + (double)s2[i].y;
+        }
+    } else {
+        for (uint32_t base = vlo + threadIdx.x; base < vhi; base += kThreads * kUnroll) {
+            float f[kUnroll][V];
+    #pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint32_t v = base + u * kThreads;
+                if (v < vhi) {
+                    const uint32_t j = v * V;
+                    const uint32_t n = fdiv(j, fd_hw);
+                    const T* p = xc + ((int64_t)n * C) * HW + (j - n * (uint32_t)HW);
+                    if constexpr (VEC) {
+                        unpack<T>(ld_vec(p), f[u]);
+                    } else {
+                        f[u][0] = ld_scalar<T>(p);
+                    }
                 } else {
-                    f[u][0] = ld_scalar<T>(p);
+    #pragma unroll
+                    for (int k = 0; k < V; ++k) f[u][k] = K;
                 }
-            } else {
-#pragma unroll
-                for (int k = 0; k < V; ++k) f[u][k] = K;
+            }
+    #pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+    #pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    const float dv = f[u][k] - K;
+                    a1[k] += dv;
+                    a2[k] = fmaf(dv, dv, a2[k]);
+                }
+            if (++iter == 16) {
+                iter = 0;
+    #pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    d1 += a1[k];
+                    d2 += a2[k];
+                    a1[k] = a2[k] = 0.f;
+                }
             }
         }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-                const float dv = f[u][k] - K;
-                a1[k] += dv;
-                a2[k] = fmaf(dv, dv, a2[k]);
-            }
-        if (++iter == 16) {
-            iter = 0;
-#pragma unroll
-            for (int k = 0; k < V; ++k) {
-                d1 += a1[k];
-                d2 += a2[k];
-                a1[k] = a2[k] = 0.f;
-            }
+    #pragma unroll
+        for (int k = 0; k < V; ++k) {
+            d1 += a1[k];
+            d2 += a2[k];
         }
-    }
-#pragma unroll
-    for (int k = 0; k < V; ++k) {
-        d1 += a1[k];
-        d2 += a2[k];
     }
     double v2[2] = {d1, d2};
     block_sum<2>(v2, red);
@@ -363,6 +452,71 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// F2 for NCHW with HW*b a multiple of 16 (the usual case): a grid-stride walk
+// over 16-byte vectors (the whole grid sweeps one contiguous window at a time)
+// with a (plane offset, channel) cursor advanced by the fixed stride -- no
+// divisions in the loop -- and kUnroll loads issued before the math.
+// y = (x - mu_hi) A + (beta - mu_lo A), z = max(y, a y).
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
+                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope) {
+    constexpr int V = Elem<T>::kVec;
+    constexpr int NP = Pairs<T>::kN;
+    const uint32_t stride = gridDim.x * kThreads;  // vectors
+    uint32_t v = blockIdx.x * kThreads + threadIdx.x;
+    if (v >= nvec) return;
+    // cursor of element e = v V: plane offset sp, channel c; one stride = q planes + rr
+    const uint32_t se = stride * V;
+    const uint32_t q = fdiv(se, fd_hw), rr = se - q * HW;
+    const uint32_t qc = q - fdiv(q, fd_c) * C;
+    uint32_t row = fdiv(v * V, fd_hw);
+    uint32_t sp = v * V - row * HW;
+    uint32_t c = row - fdiv(row, fd_c) * C;
+    const float2 sl2 = make_float2(slope, slope);
+    auto apply = [&](const uint4 r, const uint32_t cc, const uint32_t vv) {
+        const float4 cf = __ldg(coef + cc);  // (A, mu_hi, mu_lo, beta)
+        const float bp = fmaf(-cf.z, cf.x, cf.w);
+        const float2 A2 = make_float2(cf.x, cf.x), B2 = make_float2(bp, bp);
+        float2 w[NP];
+        Pairs<T>::load_sub(r, cf.y, w);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            const float2 y = fma2(w[i], A2, B2);
+            const float2 ay = mul2(y, sl2);
+            w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+        }
+        st_vec(z + (size_t)vv * V, Pairs<T>::store(w));
+    };
+    auto advance = [&]() {
+        v += stride;
+        sp += rr;
+        const bool carry = sp >= HW;
+        sp = carry ? sp - HW : sp;
+        c += qc + (carry ? 1u : 0u);
+        c = c >= C ? c - C : c;
+    };
+    for (; v + (kUnroll - 1) * stride < nvec;) {
+        uint4 r[kUnroll];
+        uint32_t cu[kUnroll], vu[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            r[u] = ld_vec(x + (size_t)v * V);
+            cu[u] = c;
+            vu[u] = v;
+            advance();
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) apply(r[u], cu[u], vu[u]);
+    }
+    for (; v < nvec;) {
+        const uint4 r = ld_vec(x + (size_t)v * V);
+        const uint32_t cc = c, vv = v;
+        advance();
+        apply(r, cc, vv);
+    }
+}
+
 // ====================================================================== B1: gradient sums
 // Per element (Alg. 2 l.2-5): dy = f'(z) dz, y = f^-1(z),
 // x^ = (y - beta)/g = y * inv_g + nb;  per channel S1 = sum dy, S2 = sum dy x^.
@@ -403,43 +557,90 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
     double d1 = 0.0, d2 = 0.0;
     int iter = 0;
-    for (uint32_t base = vlo + threadIdx.x; base < vhi; base += kThreads * kUnroll) {
-        float fz[kUnroll][V], fd[kUnroll][V];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const uint32_t v = base + u * kThreads;
-            if (v < vhi) {
-                const uint32_t j = v * V;
-                const uint32_t n = fdiv(j, fd_hw);
-                const int64_t off = ((int64_t)n * C) * HW + (j - n * (uint32_t)HW);
-                if constexpr (VEC) {
-                    unpack<T>(ld_vec(zc + off), fz[u]);
-                    unpack<T>(ld_vec(dzc + off), fd[u]);
-                } else {
-                    fz[u][0] = ld_scalar<T>(zc + off);
-                    fd[u][0] = ld_scalar<T>(dzc + off);
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < V; ++k) fz[u][k] = fd[u][k] = 0.f;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
+    if constexpr (VEC) {
+        // raw 16-byte loads of z and dz first (2 x kUnroll in flight), plane cursor
+        const int64_t CHW = C * HW;
+        const uint32_t step = kThreads * V;
+        uint32_t v = vlo + threadIdx.x;
+        PlaneCursor cur;
+        cur.seek(v * V, fd_hw, (uint32_t)HW, CHW);
+        auto accumulate = [&](const uint4 rz, const uint4 rd) {
+            float fz[V], fd[V];
+            unpack<T>(rz, fz);
+            unpack<T>(rd, fd);
 #pragma unroll
             for (int k = 0; k < V; ++k) {
                 float dy, xh;
-                grad_terms(fz[u][k], fd[u][k], slope, inv_slope, ia, dy, xh);
+                grad_terms(fz[k], fd[k], slope, inv_slope, ia, dy, xh);
                 a1[k] += dy;
                 a2[k] = fmaf(dy, xh, a2[k]);
             }
-        if (++iter == 16) {
-            iter = 0;
+        };
+        for (; v + (kUnroll - 1) * kThreads < vhi;) {
+            uint4 rz[kUnroll], rd[kUnroll];
 #pragma unroll
-            for (int k = 0; k < V; ++k) {
-                d1 += a1[k];
-                d2 += a2[k];
-                a1[k] = a2[k] = 0.f;
+            for (int u = 0; u < kUnroll; ++u) {
+                rz[u] = ld_vec_ro(zc + cur.off);
+                rd[u] = ld_vec_ro(dzc + cur.off);
+                v += kThreads;
+                cur.next(step, v * V, fd_hw, (uint32_t)HW, CHW);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) accumulate(rz[u], rd[u]);
+            if (++iter == 16) {
+                iter = 0;
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    d1 += a1[k];
+                    d2 += a2[k];
+                    a1[k] = a2[k] = 0.f;
+                }
+            }
+        }
+        for (; v < vhi;) {
+            accumulate(ld_vec_ro(zc + cur.off), ld_vec_ro(dzc + cur.off));
+            v += kThreads;
+            cur.next(step, v * V, fd_hw, (uint32_t)HW, CHW);
+        }
+    } else {
+        for (uint32_t base = vlo + threadIdx.x; base < vhi; base += kThreads * kUnroll) {
+            float fz[kUnroll][V], fd[kUnroll][V];
+    #pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const uint32_t v = base + u * kThreads;
+                if (v < vhi) {
+                    const uint32_t j = v * V;
+                    const uint32_t n = fdiv(j, fd_hw);
+                    const int64_t off = ((int64_t)n * C) * HW + (j - n * (uint32_t)HW);
+                    if constexpr (VEC) {
+                        unpack<T>(ld_vec(zc + off), fz[u]);
+                        unpack<T>(ld_vec(dzc + off), fd[u]);
+                    } else {
+                        fz[u][0] = ld_scalar<T>(zc + off);
+                        fd[u][0] = ld_scalar<T>(dzc + off);
+                    }
+                } else {
+    #pragma unroll
+                    for (int k = 0; k < V; ++k) fz[u][k] = fd[u][k] = 0.f;
+                }
+            }
+    #pragma unroll
+            for (int u = 0; u < kUnroll; ++u)
+    #pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    float dy, xh;
+                    grad_terms(fz[u][k], fd[u][k], slope, inv_slope, ia, dy, xh);
+                    a1[k] += dy;
+                    a2[k] = fmaf(dy, xh, a2[k]);
+                }
+            if (++iter == 16) {
+                iter = 0;
+    #pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    d1 += a1[k];
+                    d2 += a2[k];
+                    a1[k] = a2[k] = 0.f;
+                }
             }
         }
     }

@@ -265,3 +265,14 @@ def test_large_beta_over_gamma(flags):
     got = run_gpu(case, x, dz, p, flags=flags)
     ref = run_oracle(case, x, dz, p)
     compare(case, got, ref, p)
+
+
+# ------------------------------------------------------------------ streaming kernels at large planes
+@pytest.mark.parametrize("case", [
+    Case(3, 5, 64 * 64, dtype="bf16", seed=16),  # bf16, HW >= kThreads * 8: row-cursor apply
+    Case(2, 7, 1100, dtype="f32", seed=17),      # f32, HW >= kThreads * 4, ragged plane / thread
+    Case(5, 3, 2056, dtype="bf16", seed=18),     # plane not a multiple of the thread step
+], ids=["bf16_4096", "f32_1100", "bf16_2056"])
+@pytest.mark.parametrize("flags", [0, STREAM], ids=["auto", "streaming"])
+def test_large_planes(case, flags):
+    _check(case, flags)
