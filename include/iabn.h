@@ -202,6 +202,27 @@ IABN_API iabn_status iabn_backward_apply(const iabn_desc *desc, const void *z, c
                                 float *dgamma, float *dbeta, float eps, float slope,
                                 uint32_t flags, void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------ test time
+ * Absorb the test-time BN of a Conv layer's output channels into the Conv's
+ * weights and bias ("absorbing BN parameters into the preceding
+ * Conv layer ... at test-time BN becomes a linear operation").
+ * Per output channel k, with s_k = g_k / sqrt(running_var_k + eps) and g the
+ * effective scale of the flags (|gamma|+eps default, gamma with GAMMA_PLAIN, 1
+ * with GAMMA_FIXED_ONE):
+ *   w_out[k][j] = s_k * w[k][j]                 (j < k_per_out, row-major [cout][k])
+ *   bias_out[k] = s_k * (bias[k] - running_mean[k]) + beta[k]     (bias NULL = 0)
+ * so that conv(x; w_out, bias_out) = BN_eval(conv(x; w, bias)).  The activation
+ * is not folded (it is not linear).  All pointers are fp32 DEVICE arrays; w_out
+ * may be w and bias_out may be bias (in place), any other overlap is
+ * IABN_ERR_ALIAS.  Errors: IABN_ERR_INVALID_ARG (NULL required pointer, cout or
+ * k_per_out <= 0, eps <= 0 or non-finite), IABN_ERR_UNSUPPORTED (misaligned w
+ * / w_out: 16 bytes), IABN_ERR_CUDA.  s_k is formed in fp64, then rounded. */
+IABN_API iabn_status iabn_fold_conv(int64_t cout, int64_t k_per_out, const float *w,
+                                    const float *bias, const float *running_mean,
+                                    const float *running_var, const float *gamma,
+                                    const float *beta, float eps, uint32_t flags, float *w_out,
+                                    float *bias_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

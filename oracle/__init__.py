@@ -57,9 +57,10 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
     for f in (lib.oracle_backward_inplace_I, lib.oracle_backward_inplace_II):
         f.argtypes = [_I64, _I64, _I64, i, _D, _D, _D, _D, _D, i, d, d, _D, _D, _D]
     lib.oracle_merge_stats.argtypes = [_I64, _I64, _D, _D, _D, _D, _D, _D]
+    lib.oracle_fold_conv.argtypes = [_I64, _I64, _D, _D, _D, _D, _D, _D, i, d, _D, _D]
     for f in (lib.oracle_channel_stats, lib.oracle_forward, lib.oracle_forward_eval,
               lib.oracle_backward_standard, lib.oracle_backward_inplace_I,
-              lib.oracle_backward_inplace_II, lib.oracle_merge_stats):
+              lib.oracle_backward_inplace_II, lib.oracle_merge_stats, lib.oracle_fold_conv):
         f.restype = None
     lib.oracle_mutant_id.restype = ctypes.c_int
     return lib
@@ -137,6 +138,21 @@ class Oracle:
                                      _p(_f64(beta)), GAMMA_MODES[gamma_mode], eps, slope,
                                      _p(_f64(running_mean)), _p(_f64(running_var)), _p(z))
         return z
+
+    def fold_conv(self, w, bias, running_mean, running_var, gamma, beta, *, eps=1e-5,
+                  gamma_mode="abs_eps"):
+        """Test-time BN absorbed into the preceding conv: w [cout, ...],
+        bias [cout] or None -> (w', bias')."""
+        w = _f64(w)
+        cout = w.shape[0]
+        kper = int(w.size // cout)
+        w_out, b_out = np.empty_like(w), np.empty(cout)
+        b = None if bias is None else _f64(bias)
+        self.lib.oracle_fold_conv(cout, kper, _p(w), None if b is None else _p(b),
+                                  _p(_f64(running_mean)), _p(_f64(running_var)), _p(_f64(gamma)),
+                                  _p(_f64(beta)), GAMMA_MODES[gamma_mode], eps, _p(w_out),
+                                  _p(b_out))
+        return w_out, b_out
 
     def backward_standard(self, x, dz, gamma, beta, *, eps=1e-5, slope=0.01,
                           gamma_mode="abs_eps", layout="NCHW"):

@@ -381,4 +381,32 @@ void oracle_merge_stats(int64_t K, int64_t C, const double *counts, const double
     }
 }
 
+/*
+ * Test-time folding: "the computation of networks trained with
+ * batch normalization can be sped up by absorbing BN parameters into the
+ * preceding Conv layer, by performing a simple update of the convolution
+ * weights and biases.  This is possible because at test-time BN becomes a
+ * linear operation."  With fixed statistics mu_T, sigma_T^2 the BN of output
+ * channel k is y = g_k (v - mu_k)/sqrt(sigma_k^2 + eps) + beta_k, v = w_k . x + b_k, so
+ *   w'_k = s_k w_k,  b'_k = s_k (b_k - mu_k) + beta_k,  s_k = g_k / sqrt(sigma_k^2 + eps)
+ * (SPEC.md:239-247).  w is [cout][kper] row-major; bias NULL means 0.
+ */
+void oracle_fold_conv(int64_t cout, int64_t kper, const double *w, const double *bias,
+                      const double *running_mean, const double *running_var,
+                      const double *gamma, const double *beta, int gamma_mode, double eps,
+                      double *w_out, double *bias_out)
+{
+    for (int64_t k = 0; k < cout; ++k) {
+        const double s = gamma_eff(gamma_mode, gamma[k], eps) / sqrt(running_var[k] + eps);
+        for (int64_t j = 0; j < kper; ++j)
+            w_out[k * kper + j] = s * w[k * kper + j];
+        const double b = bias ? bias[k] : 0.0;
+#if ORACLE_MUTANT == 11
+        bias_out[k] = s * b + beta[k]; /* forgot the running mean */
+#else
+        bias_out[k] = s * (b - running_mean[k]) + beta[k];
+#endif
+    }
+}
+
 int oracle_mutant_id(void) { return ORACLE_MUTANT; }

@@ -39,5 +39,9 @@ void oracle_backward_inplace_II(int64_t N, int64_t C, int64_t HW, int layout, co
 void oracle_merge_stats(int64_t K, int64_t C, const double *counts, const double *means,
                         const double *vars, double *count_out, double *mean_out,
                         double *var_out);
+void oracle_fold_conv(int64_t cout, int64_t kper, const double *w, const double *bias,
+                      const double *running_mean, const double *running_var,
+                      const double *gamma, const double *beta, int gamma_mode, double eps,
+                      double *w_out, double *bias_out);
 int oracle_mutant_id(void);
 #endif

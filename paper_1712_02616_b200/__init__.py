@@ -6,9 +6,9 @@ behind the C ABI of include/iabn.h.  This package is its thin Python binding.
 """
 from . import _lib
 from .functional import (Comm, InPlaceABN, InPlaceABNFunction, backward, backward_apply,
-                         backward_reduce, forward, forward_apply, forward_reduce, inplace_abn,
-                         layout_of)
+                         backward_reduce, fold_conv, forward, forward_apply, forward_reduce,
+                         inplace_abn, layout_of)
 
 __all__ = ["Comm", "InPlaceABN", "InPlaceABNFunction", "backward", "backward_apply",
-           "backward_reduce", "forward", "forward_apply", "forward_reduce", "inplace_abn",
+           "backward_reduce", "fold_conv", "forward", "forward_apply", "forward_reduce", "inplace_abn",
            "layout_of", "_lib"]

@@ -32,7 +32,7 @@ EXPORTS = ["iabn_version", "iabn_status_string", "iabn_last_error", "iabn_launch
            "iabn_workspace_bytes", "iabn_query_schedule", "iabn_forward", "iabn_backward",
            "iabn_comm_get_unique_id", "iabn_comm_init", "iabn_comm_destroy", "iabn_forward_sync",
            "iabn_backward_sync", "iabn_forward_reduce", "iabn_forward_apply",
-           "iabn_backward_reduce", "iabn_backward_apply"]
+           "iabn_backward_reduce", "iabn_backward_apply", "iabn_fold_conv"]
 
 
 class Desc(ctypes.Structure):
@@ -82,6 +82,8 @@ def _load() -> ctypes.CDLL:
     lib.iabn_backward_reduce.argtypes = [_DP, _P, _P, _P, _P, _P, _F, _F, _U32, _P, _SZ, _P]
     lib.iabn_backward_apply.argtypes = [_DP, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _F, _F, _U32,
                                         _P, _SZ, _P]
+    lib.iabn_fold_conv.argtypes = [ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _F,
+                                   _U32, _P, _P, _P]
     for name in EXPORTS:
         if name not in ("iabn_version", "iabn_status_string", "iabn_last_error",
                         "iabn_launch_count", "iabn_workspace_bytes"):

@@ -869,6 +869,34 @@ iabn_status iabn_backward(const iabn_desc* desc, const void* z, const void* dz, 
                     eps, slope, flags);
 }
 
+// ---------------------------------------------------------------- test time
+iabn_status iabn_fold_conv(int64_t cout, int64_t k_per_out, const float* w, const float* bias,
+                           const float* running_mean, const float* running_var,
+                           const float* gamma, const float* beta, float eps, uint32_t flags,
+                           float* w_out, float* bias_out, void* stream) {
+    if (cout <= 0 || k_per_out <= 0)
+        return fail(IABN_ERR_INVALID_ARG, "cout and k_per_out must be positive");
+    if (cout > 0x7fffffffll) return fail(IABN_ERR_UNSUPPORTED, "cout too large");
+    if (!w || !w_out || !running_mean || !running_var || !gamma || !beta || !bias_out)
+        return fail(IABN_ERR_INVALID_ARG, "NULL required pointer");
+    if (!(eps > 0.f) || !std::isfinite(eps))
+        return fail(IABN_ERR_INVALID_ARG, "eps must be finite and > 0 (got %g)", (double)eps);
+    if (!aligned16(w) || !aligned16(w_out))
+        return fail(IABN_ERR_UNSUPPORTED, "w / w_out not 16-byte aligned");
+    const size_t wb = (size_t)cout * (size_t)k_per_out * sizeof(float), cb = (size_t)cout * 4;
+    IABN_TRY(check_same_or_disjoint("w", w, "w_out", w_out, wb));
+    if (bias) IABN_TRY(check_same_or_disjoint("bias", bias, "bias_out", bias_out, cb));
+    {
+        const uintptr_t a0 = (uintptr_t)w_out, b0 = (uintptr_t)bias_out;
+        if (a0 < b0 + cb && b0 < a0 + wb) return fail(IABN_ERR_ALIAS, "w_out and bias_out overlap");
+    }
+    DevFacts* dev = nullptr;
+    IABN_TRY(device_facts(&dev));
+    fold_conv_kernel<<<(unsigned)cout, kThreads, 0, (cudaStream_t)stream>>>(
+        w, bias, running_mean, running_var, gamma, beta, eps, flags, k_per_out, w_out, bias_out);
+    return check_launch("fold_conv kernel");
+}
+
 // ---------------------------------------------------------------- split phase
 iabn_status iabn_forward_reduce(const iabn_desc* desc, const void* x, double* stats, void* ws,
                                 size_t ws_bytes, void* stream) {

@@ -859,4 +859,25 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// ====================================================================== test-time folding
+// BN at test time is linear and is absorbed into the preceding Conv.
+// Block k scales row k of w (k_per_out values) by s_k = g_k / sqrt(rv_k + eps) and
+// writes bias'_k = s_k (bias_k - rm_k) + beta_k.
+__global__ void __launch_bounds__(kThreads)
+    fold_conv_kernel(const float* w, const float* bias, const float* __restrict__ rm,
+                     const float* __restrict__ rv, const float* __restrict__ gamma,
+                     const float* __restrict__ beta, float eps, uint32_t flags, int64_t kper,
+                     float* w_out, float* bias_out) {
+    const int64_t k = blockIdx.x;
+    const double sd = gamma_eff(gamma[k], eps, flags) / sqrt((double)rv[k] + (double)eps);
+    const float s = (float)sd;
+    const float* src = w + k * kper;
+    float* dst = w_out + k * kper;
+    for (int64_t j = threadIdx.x; j < kper; j += kThreads) dst[j] = src[j] * s;
+    if (threadIdx.x == 0) {
+        const double b = bias ? (double)bias[k] : 0.0;
+        bias_out[k] = (float)(sd * (b - (double)rm[k]) + (double)beta[k]);
+    }
+}
+
 }  // namespace iabn

@@ -254,6 +254,29 @@ def backward_apply(z, dz, sums_global, sums_local, gamma, beta, save_var, *, eps
     return dx, dgamma, dbeta
 
 
+def fold_conv(weight: torch.Tensor, bias: torch.Tensor | None, running_mean: torch.Tensor,
+              running_var: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, *,
+              eps: float = 1e-5, gamma_mode: str = "abs_eps", inplace: bool = False,
+              stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Test-time BN of a conv's output channels absorbed into the conv (PAPER.md:85,
+    iabn_fold_conv): returns (weight', bias') with conv(x; weight', bias') =
+    BN_eval(conv(x; weight, bias)).  weight: contiguous CUDA float32 [cout, ...]."""
+    if weight.dtype != torch.float32 or not weight.is_cuda or not weight.is_contiguous():
+        raise ValueError("weight must be a contiguous CUDA float32 tensor")
+    cout = weight.shape[0]
+    kper = weight.numel() // cout
+    for name, t in (("running_mean", running_mean), ("running_var", running_var),
+                    ("gamma", gamma), ("beta", beta), ("bias", bias)):
+        _f32(t, cout, name)
+    w_out = weight if inplace else torch.empty_like(weight)
+    b_out = bias if (inplace and bias is not None) else torch.empty(cout, dtype=torch.float32,
+                                                                    device=weight.device)
+    L.call("iabn_fold_conv", cout, kper, _ptr(weight), _ptr(bias), _ptr(running_mean),
+           _ptr(running_var), _ptr(gamma), _ptr(beta), eps, _flags(gamma_mode), _ptr(w_out),
+           _ptr(b_out), _stream(stream))
+    return w_out, b_out
+
+
 def schedule(x_shape_desc: L.Desc, pass_: int, flags: int = 0) -> tuple[str, int]:
     s, k = L.query_schedule(x_shape_desc, pass_, flags)
     return ("fused" if s == 1 else "streaming"), k

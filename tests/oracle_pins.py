@@ -15,6 +15,8 @@ What pins what:
   dx_moments         closed forms: sum_c dx = 0, sum_c dx*x^ = g*rstd*dg*eps/(var+eps)
   scaling            metamorphic: x -> 2^k x, eps -> 4^k eps leaves z, scales dx by 2^-k
   sync_concat        merged shard stats == stats of the concatenated batch
+  golden_fold        SPEC.md folding examples (identity BN, beta shift)
+  fold_conv          library routine: torch float64 conv2d(w', b') == batch_norm(eval)(conv2d(w, b))
 """
 from __future__ import annotations
 
@@ -312,6 +314,40 @@ def pin_permute_batch(o):
     assert chan_err(dxp, dx[perm], 1) < 1e-12
 
 
+# ---------------------------------------------------------------- test-time folding
+def pin_golden_fold(o):
+    g = _golden()
+    for key in ("fold_identity", "fold_beta_shift"):
+        e = g[key]
+        eps = 1e-5
+        w_out, b_out = o.fold_conv(np.array(e["w"]), np.array(e["bias"]),
+                                   np.array([e["running_mean"]]),
+                                   np.array([e["running_var_plus_eps"] - eps]),
+                                   np.array([e["gamma"]]), np.array([e["beta"]]), eps=eps,
+                                   gamma_mode="plain")
+        assert np.abs(w_out - np.array(e["w_out"])).max() < 1e-12, key
+        assert np.abs(b_out - np.array(e["bias_out"])).max() < 1e-12, key
+
+
+def pin_fold_conv(o):
+    rng = np.random.default_rng(11)
+    for kh, with_bias in ((3, True), (1, False)):
+        x = rng.normal(size=(2, 3, 6, 5))
+        w = rng.normal(size=(4, 3, kh, kh))
+        b = rng.normal(size=4) if with_bias else None
+        gamma = rng.uniform(0.5, 1.5, 4) * np.array([1, -1, 1, 1])
+        beta, rm = rng.normal(size=4), rng.normal(size=4)
+        rv = rng.uniform(0.2, 3.0, 4)
+        w2, b2 = o.fold_conv(w, b, rm, rv, gamma, beta, eps=1e-5)
+        v = F.conv2d(torch.tensor(x), torch.tensor(w), None if b is None else torch.tensor(b))
+        two_stage = F.batch_norm(v, torch.tensor(rm), torch.tensor(rv),
+                                 weight=torch.tensor(np.abs(gamma) + 1e-5),
+                                 bias=torch.tensor(beta), training=False, eps=1e-5)
+        folded = F.conv2d(torch.tensor(x), torch.tensor(w2), torch.tensor(b2))
+        assert (folded - two_stage).abs().max().item() < 1e-12 * max(1.0, two_stage.abs().max().item())
+
+
 PINS = [pin_golden_bn, pin_golden_leaky, pin_golden_running, pin_golden_sync, pin_whitening,
         pin_const_dz, pin_dx_moments, pin_torch_f64, pin_torch_eval, pin_finite_diff,
-        pin_three_way, pin_fixed_one, pin_scaling, pin_sync_concat, pin_permute_batch]
+        pin_three_way, pin_fixed_one, pin_scaling, pin_sync_concat, pin_permute_batch,
+        pin_golden_fold, pin_fold_conv]

@@ -143,3 +143,28 @@ def test_eval_needs_running_stats():
 @no_gpu
 def test_launch_count_is_zero_without_launches():
     assert L.launch_count() == 0
+
+
+def _fold(cout=4, k=27, w=P, bias=P * 2, rm=P * 3, rv=P * 4, gamma=P * 5, beta=P * 6, eps=1e-5,
+          flags=0, w_out=P * 64, b_out=P * 128):
+    return L.lib.iabn_fold_conv(cout, k, w, bias, rm, rv, gamma, beta, eps, flags, w_out, b_out,
+                                None)
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(cout=0), L.ERR_INVALID_ARG), (dict(k=-1), L.ERR_INVALID_ARG),
+    (dict(w=0), L.ERR_INVALID_ARG), (dict(rv=0), L.ERR_INVALID_ARG),
+    (dict(b_out=0), L.ERR_INVALID_ARG), (dict(eps=0.0), L.ERR_INVALID_ARG),
+    (dict(eps=float("nan")), L.ERR_INVALID_ARG), (dict(w=P + 4), L.ERR_UNSUPPORTED),
+    (dict(w_out=P + 16), L.ERR_ALIAS),  # partial overlap of w and w_out
+    (dict(b_out=P * 64 + 8), L.ERR_ALIAS),  # bias_out inside w_out
+    (dict(b_out=P * 2 + 4), L.ERR_ALIAS),  # partial overlap of bias and bias_out
+])
+def test_fold_conv_validation(kw, status):
+    assert _fold(**kw) == status, L.lib.iabn_last_error()
+
+
+@no_gpu
+def test_fold_conv_in_place_reaches_device():
+    assert _fold(w_out=P, b_out=P * 2) in (L.ERR_CUDA, L.OK)
+    assert _fold(bias=0) in (L.ERR_CUDA, L.OK)  # no conv bias

@@ -276,3 +276,34 @@ def test_large_beta_over_gamma(flags):
 @pytest.mark.parametrize("flags", [0, STREAM], ids=["auto", "streaming"])
 def test_large_planes(case, flags):
     _check(case, flags)
+
+
+# ------------------------------------------------------------------ test-time folding
+@pytest.mark.parametrize("gamma_mode", ["abs_eps", "plain", "fixed_one"])
+@pytest.mark.parametrize("with_bias", [True, False], ids=["bias", "nobias"])
+def test_fold_conv(gamma_mode, with_bias, orc):
+    import numpy as np
+    import paper_1712_02616_b200 as P
+    g = torch.Generator().manual_seed(19)
+    cout, shape = 37, (37, 19, 3, 3)
+    w = torch.randn(shape, generator=g)
+    b = torch.randn(cout, generator=g) if with_bias else None
+    gamma = torch.rand(cout, generator=g) + 0.5
+    gamma[::3] *= -1
+    beta, rm = torch.randn(cout, generator=g), torch.randn(cout, generator=g)
+    rv = torch.rand(cout, generator=g) * 3 + 0.1
+    dev = torch.device("cuda", 0)
+    cu = lambda t: None if t is None else t.to(dev)
+    w2, b2 = P.fold_conv(cu(w), cu(b), cu(rm), cu(rv), cu(gamma), cu(beta), gamma_mode=gamma_mode)
+    rw, rb = orc.fold_conv(w.numpy(), None if b is None else b.numpy(), rm.numpy(), rv.numpy(),
+                           gamma.numpy(), beta.numpy(), eps=1e-5, gamma_mode=gamma_mode)
+    w2, b2 = w2.cpu().double().numpy(), b2.cpu().double().numpy()
+    assert np.abs(w2 - rw).max() / np.abs(rw).max() < 1e-6
+    assert np.abs(b2 - rb).max() / np.abs(rb).max() < 1e-6
+    # in place gives the same bits
+    wi, bi = cu(w.clone()), cu(b.clone()) if b is not None else None
+    wo, bo = P.fold_conv(wi, bi, cu(rm), cu(rv), cu(gamma), cu(beta), gamma_mode=gamma_mode,
+                         inplace=True)
+    assert wo.data_ptr() == wi.data_ptr()
+    assert torch.equal(wo.cpu(), torch.from_numpy(w2).float())
+    assert torch.equal(bo.cpu(), torch.from_numpy(b2).float())
