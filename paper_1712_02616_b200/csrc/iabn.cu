@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 #include <string>
 
 #include "iabn.h"
@@ -492,6 +493,17 @@ int apply_grid(int64_t E, int b, int sms) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8));
 }
 
+// NHWC aligned: a grid whose stride (grid * kThreads vectors) is a multiple of the
+// C/V vectors of one row, so every thread keeps one channel group (0 = not possible)
+int nhwc_grid(const Geom& g, int64_t nvec, int sms) {
+    const int64_t cv = g.C * g.b / 16;
+    const int64_t q = cv / std::gcd<int64_t>(cv, kThreads);  // grid must be a multiple of q
+    const int64_t want = std::min<int64_t>((nvec + kThreads * kUnroll - 1) / (kThreads * kUnroll),
+                                           (int64_t)sms * 8);
+    if (q > (int64_t)sms * 16) return 0;
+    return (int)(std::max<int64_t>(1, (want + q - 1) / q) * q);
+}
+
 template <typename T>
 iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4* coef,
                              float slope, int sms, cudaStream_t st) {
@@ -514,6 +526,9 @@ iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4
                 fwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
             else
                 fwd_apply_kernel<T, 0, false><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+        } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
+            fwd_apply_nhwc_kernel<T><<<nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st>>>(
+                xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope);
         } else {
             if (al)
                 fwd_apply_kernel<T, 1, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
@@ -546,6 +561,10 @@ iabn_status launch_bwd_apply(const Geom& g, const void* z, const void* dz, void*
                 bwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
             else
                 bwd_apply_kernel<T, 0, false><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+        } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
+            bwd_apply_nhwc_kernel<T><<<nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st>>>(
+                zp, dzp, dxp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope,
+                inv_slope);
         } else {
             if (al)
                 bwd_apply_kernel<T, 1, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
@@ -558,6 +577,8 @@ iabn_status launch_bwd_apply(const Geom& g, const void* z, const void* dz, void*
 }
 
 unsigned cgrid(int64_t C) { return (unsigned)((C + 127) / 128); }
+// warp-per-channel kernels (combine / coefficients), 128 threads = 4 channels per block
+unsigned wgrid(int64_t C) { return (unsigned)((C + 3) / 4); }
 
 // ====================================================================== NCCL (dlopen)
 struct Nccl {
@@ -691,7 +712,7 @@ iabn_status fwd_from_partials(const Ctx& c, const double* part, int S, const voi
                               uint32_t flags) {
     FwdCoefArgs a{part, S, c.g.C, gamma, beta, rm, rv, sm, sv, wsp<float4>(c, c.w.coef),
                   momentum, eps, flags};
-    fwd_coef_kernel<<<cgrid(c.g.C), 128, 0, c.st>>>(a);
+    fwd_coef_kernel<<<wgrid(c.g.C), 128, 0, c.st>>>(a);
     IABN_TRY(check_launch("fwd_coef kernel"));
     return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
 }
@@ -743,7 +764,7 @@ iabn_status bwd_from_sums(const Ctx& c, const double* glob, int Sg, const double
                           float* dg, float* db, float eps, float slope, uint32_t flags) {
     BwdCoefArgs a{glob, Sg, loc, Sl, count_ptr, count, c.g.C, gamma, beta, sv, dg, db,
                   wsp<float4>(c, c.w.coef), eps, flags};
-    bwd_coef_kernel<<<cgrid(c.g.C), 128, 0, c.st>>>(a);
+    bwd_coef_kernel<<<wgrid(c.g.C), 128, 0, c.st>>>(a);
     IABN_TRY(check_launch("bwd_coef kernel"));
     return launch_bwd_apply<T>(c.g, z, dz, dx, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
 }
@@ -906,7 +927,7 @@ iabn_status iabn_forward_reduce(const iabn_desc* desc, const void* x, double* st
     if (!stats) return fail(IABN_ERR_INVALID_ARG, "stats is NULL");
     IABN_TRY(attach_device(c));
     IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
-    combine_kernel<3><<<cgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
+    combine_kernel<3><<<wgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
                                                       -1.0);
     return check_launch("combine kernel");
 }
@@ -941,7 +962,7 @@ iabn_status iabn_backward_reduce(const iabn_desc* desc, const void* z, const voi
     double* part = wsp<double>(c, c.w.part);
     IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
                       flags, part, c.st));
-    combine_kernel<2><<<cgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, sums, (double)c.g.m);
+    combine_kernel<2><<<wgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, sums, (double)c.g.m);
     return check_launch("combine kernel");
 }
 
@@ -1018,7 +1039,7 @@ iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, con
     IABN_TRY(attach_device(c));
     double* stats = wsp<double>(c, c.w.stats);
     IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
-    combine_kernel<3><<<cgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
+    combine_kernel<3><<<wgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
                                                       -1.0);
     IABN_TRY(check_launch("combine kernel"));
     IABN_TRY(allreduce_f64(stats, (size_t)c.g.C * 3, comm, c.st));
@@ -1044,7 +1065,7 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
     double* glob = wsp<double>(c, c.w.sums_glob);
     IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
                       flags, part, c.st));
-    combine_kernel<2><<<cgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, loc, (double)c.g.m);
+    combine_kernel<2><<<wgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, loc, (double)c.g.m);
     IABN_TRY(check_launch("combine kernel"));
     const size_t nb = (size_t)(2 * c.g.C + 1) * sizeof(double);
     const cudaError_t e = cudaMemcpyAsync(glob, loc, nb, cudaMemcpyDeviceToDevice, c.st);

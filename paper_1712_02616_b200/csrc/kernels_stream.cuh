@@ -228,39 +228,52 @@ __global__ void __launch_bounds__(kThreads)
     for (int k = 0; k < V; ++k) d1[k] = d2[k] = 0.0;
     if (active) {
         int iter = 0;
-        for (int64_t r0 = rlo + ty; r0 < rhi; r0 += 16 * kUnroll) {
-            float f[kUnroll][V];
+        auto acc = [&](const float (&f)[V]) {
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                const int64_t r = r0 + 16 * u;
-                if (r < rhi) {
-                    const T* p = x + r * C + c0;
-                    if constexpr (VEC) {
-                        unpack<T>(ld_vec(p), f[u]);
-                    } else {
-                        f[u][0] = ld_scalar<T>(p);
-                    }
-                } else {
+            for (int k = 0; k < V; ++k) {
+                const float dv = f[k] - K[k];
+                a1[k] += dv;
+                a2[k] = fmaf(dv, dv, a2[k]);
+            }
+        };
+        auto flush = [&]() {
 #pragma unroll
-                    for (int k = 0; k < V; ++k) f[u][k] = K[k];
+            for (int k = 0; k < V; ++k) {
+                d1[k] += a1[k];
+                d2[k] += a2[k];
+                a1[k] = a2[k] = 0.f;
+            }
+        };
+        int64_t r0 = rlo + ty;
+        if constexpr (VEC) {
+            // raw loads of kStatUnroll rows first (all in range), then the math
+            for (; r0 + 16 * (kStatUnroll - 1) < rhi; r0 += 16 * kStatUnroll) {
+                uint4 raw[kStatUnroll];
+#pragma unroll
+                for (int u = 0; u < kStatUnroll; ++u) raw[u] = ld_vec_ro(x + (r0 + 16 * u) * C + c0);
+#pragma unroll
+                for (int u = 0; u < kStatUnroll; ++u) {
+                    float f[V];
+                    unpack<T>(raw[u], f);
+                    acc(f);
+                }
+                if (++iter == 4) {
+                    iter = 0;
+                    flush();
                 }
             }
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    const float dv = f[u][k] - K[k];
-                    a1[k] += dv;
-                    a2[k] = fmaf(dv, dv, a2[k]);
-                }
-            if (++iter == 16) {
+        }
+        for (; r0 < rhi; r0 += 16) {
+            float f[V];
+            if constexpr (VEC) {
+                unpack<T>(ld_vec_ro(x + r0 * C + c0), f);
+            } else {
+                f[0] = ld_scalar<T>(x + r0 * C + c0);
+            }
+            acc(f);
+            if (++iter == 64) {
                 iter = 0;
-#pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    d1[k] += a1[k];
-                    d2[k] += a2[k];
-                    a1[k] = a2[k] = 0.f;
-                }
+                flush();
             }
         }
     }
@@ -287,21 +300,39 @@ __global__ void __launch_bounds__(kThreads)
 
 // Sum S partial records of NV doubles per channel in fixed order: out[c][k].
 // extra >= 0: out[NV*C] = extra (the count slot of the backward sums).
+// Sum over the S split records of channel c: lane l of the channel's warp takes
+// splits l, l+32, ... in order, then a fixed xor tree -- parallel and still the
+// same order every run (bitwise reproducible).
+template <int NV>
+__device__ __forceinline__ void warp_split_sum(const double* __restrict__ part, int S, int64_t C,
+                                               int64_t c, double (&acc)[NV]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    for (int s = lane; s < S; s += 32)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) acc[k] += part[((int64_t)s * C + c) * NV + k];
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+}
+// one warp per channel: blockDim.x = 128 -> 4 channels per block
+__device__ __forceinline__ int64_t warp_channel() {
+    return (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+}
+
 template <int NV>
 __global__ void combine_kernel(const double* __restrict__ part, int S, int64_t C,
                                double* __restrict__ out, double extra) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < C) {
-        double acc[NV];
-#pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-        for (int s = 0; s < S; ++s)
-#pragma unroll
-            for (int k = 0; k < NV; ++k) acc[k] += part[((int64_t)s * C + c) * NV + k];
+    const int64_t c = warp_channel();
+    if (c == 0 && threadIdx.x == 0 && extra >= 0.0) out[NV * C] = extra;
+    if (c >= C) return;
+    double acc[NV];
+    warp_split_sum<NV>(part, S, C, c, acc);
+    if ((threadIdx.x & 31) == 0)
 #pragma unroll
         for (int k = 0; k < NV; ++k) out[c * NV + k] = acc[k];
-    }
-    if (c == 0 && extra >= 0.0) out[NV * C] = extra;
 }
 
 // F1 finalize (+F1' running stats): from S partial raw moments per channel to
@@ -355,15 +386,12 @@ __device__ __forceinline__ void update_running(float* rm, float* rv, int64_t c, 
 }
 
 __global__ void fwd_coef_kernel(FwdCoefArgs a) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = warp_channel();
     if (c >= a.C) return;
-    double cnt = 0.0, sum = 0.0, sumsq = 0.0;
-    for (int s = 0; s < a.S; ++s) {
-        const double* p = a.part + ((int64_t)s * a.C + c) * 3;
-        cnt += p[0];
-        sum += p[1];
-        sumsq += p[2];
-    }
+    double acc[3];
+    warp_split_sum<3>(a.part, a.S, a.C, c, acc);
+    if (threadIdx.x & 31) return;
+    const double cnt = acc[0], sum = acc[1], sumsq = acc[2];
     double mean, var;
     a.coef[c] = fwd_coef_from_moments(cnt, sum, sumsq, a.gamma[c], a.beta[c], a.eps, a.flags,
                                       &mean, &var);
@@ -782,22 +810,18 @@ __device__ __forceinline__ float4 bwd_coef_from_sums(double S1, double S2, doubl
 }
 
 __global__ void bwd_coef_kernel(BwdCoefArgs a) {
-    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t c = warp_channel();
     if (c >= a.C) return;
-    double g1 = 0.0, g2 = 0.0, l1 = 0.0, l2 = 0.0;
-    for (int s = 0; s < a.S_glob; ++s) {
-        g1 += a.glob[((int64_t)s * a.C + c) * 2];
-        g2 += a.glob[((int64_t)s * a.C + c) * 2 + 1];
-    }
+    double gs[2], ls[2];
+    warp_split_sum<2>(a.glob, a.S_glob, a.C, c, gs);
     if (a.loc == a.glob) {
-        l1 = g1;
-        l2 = g2;
+        ls[0] = gs[0];
+        ls[1] = gs[1];
     } else {
-        for (int s = 0; s < a.S_loc; ++s) {
-            l1 += a.loc[((int64_t)s * a.C + c) * 2];
-            l2 += a.loc[((int64_t)s * a.C + c) * 2 + 1];
-        }
+        warp_split_sum<2>(a.loc, a.S_loc, a.C, c, ls);
     }
+    if (threadIdx.x & 31) return;
+    const double g1 = gs[0], g2 = gs[1], l1 = ls[0], l2 = ls[1];
     const double m = a.count_ptr ? *a.count_ptr : a.count;
     a.coef[c] = bwd_coef_from_sums(g1, g2, m, a.gamma[c], a.beta[c], a.save_var[c], a.eps, a.flags);
     a.dbeta[c] = (float)l1;
@@ -857,6 +881,95 @@ __global__ void __launch_bounds__(kThreads)
         const float dy = pos ? dd : dd * slope;
         st_scalar<T>(dx + e, fmaf(cf.x, dy, fmaf(cf.y, y, cf.z)));
     }
+}
+
+// ====================================================================== NHWC elementwise passes
+// NHWC with C*b a multiple of 16: vector v holds channels (v mod C/V)*V .. +V-1.  The
+// host sizes the grid so that the grid stride (gridDim.x*kThreads vectors) is a
+// multiple of C/V: every thread then keeps ONE channel group for the whole walk,
+// its V channels' coefficients live in registers, and the loop is pure streaming.
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    fwd_apply_nhwc_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
+                          uint32_t cv, float slope) {
+    constexpr int V = Elem<T>::kVec;
+    constexpr int NP = V / 2;
+    const uint32_t stride = gridDim.x * kThreads;
+    uint32_t v = blockIdx.x * kThreads + threadIdx.x;
+    if (v >= nvec) return;
+    const uint32_t c0 = (v % cv) * V;
+    float2 A[NP], B[NP], M[NP];  // per channel pair: A, beta - mu_lo A, mu_hi
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+        const float4 c_a = __ldg(coef + c0 + 2 * i), c_b = __ldg(coef + c0 + 2 * i + 1);
+        A[i] = make_float2(c_a.x, c_b.x);
+        B[i] = make_float2(fmaf(-c_a.z, c_a.x, c_a.w), fmaf(-c_b.z, c_b.x, c_b.w));
+        M[i] = make_float2(c_a.y, c_b.y);
+    }
+    const float2 sl2 = make_float2(slope, slope);
+    auto apply = [&](const uint4 r, const uint32_t vv) {
+        float2 w[NP];
+        Pairs<T>::load(r, w);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+            const float2 y = fma2(add2(w[i], make_float2(-M[i].x, -M[i].y)), A[i], B[i]);
+            const float2 ay = mul2(y, sl2);
+            w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+        }
+        st_vec(z + (size_t)vv * V, Pairs<T>::store(w));
+    };
+    for (; v + (kUnroll - 1) * stride < nvec; v += kUnroll * stride) {
+        uint4 r[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) r[u] = ld_vec(x + (size_t)(v + u * stride) * V);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) apply(r[u], v + u * stride);
+    }
+    for (; v < nvec; v += stride) apply(ld_vec(x + (size_t)v * V), v);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    bwd_apply_nhwc_kernel(const T* __restrict__ z, const T* dz, T* dx,
+                          const float4* __restrict__ coef, uint32_t nvec, uint32_t cv,
+                          float slope, float inv_slope) {
+    constexpr int V = Elem<T>::kVec;
+    const uint32_t stride = gridDim.x * kThreads;
+    uint32_t v = blockIdx.x * kThreads + threadIdx.x;
+    if (v >= nvec) return;
+    const uint32_t c0 = (v % cv) * V;
+    float al[V], ka[V], cc[V];  // dx = al dy + ka y + cc
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        const float4 cf = __ldg(coef + c0 + k);
+        al[k] = cf.x;
+        ka[k] = cf.y;
+        cc[k] = cf.z;
+    }
+    auto apply = [&](const uint4 rz, const uint4 rd, const uint32_t vv) {
+        float fz[V], fd[V];
+        unpack<T>(rz, fz);
+        unpack<T>(rd, fd);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const bool pos = fz[k] >= 0.f;  // -0.0 counts as >= 0
+            const float y = pos ? fz[k] : fz[k] * inv_slope;
+            const float dy = pos ? fd[k] : fd[k] * slope;
+            fz[k] = fmaf(al[k], dy, fmaf(ka[k], y, cc[k]));
+        }
+        st_vec(dx + (size_t)vv * V, pack<T>(fz));
+    };
+    for (; v + (kUnroll - 1) * stride < nvec; v += kUnroll * stride) {
+        uint4 rz[kUnroll], rd[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            rz[u] = ld_vec(z + (size_t)(v + u * stride) * V);
+            rd[u] = ld_vec(dz + (size_t)(v + u * stride) * V);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) apply(rz[u], rd[u], v + u * stride);
+    }
+    for (; v < nvec; v += stride) apply(ld_vec(z + (size_t)v * V), ld_vec(dz + (size_t)v * V), v);
 }
 
 // ====================================================================== test-time folding
