@@ -86,6 +86,9 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+SCHEDULES = ["streaming", "fused", "one-launch"]  # iabn_query_schedule codes
+
+
 def load_traffic(config: str):
     """dram read+write bytes per launch of the dominant kernel from the committed
     ncu --set full capture summary (profiles/), if one exists for this workload."""
@@ -451,8 +454,8 @@ def main():
                        "parallelism": f"dp{world}" + ("+sync-stats" if world > 1 else ""),
                        "l2": ("inputs larger than L2 (x, dz %.2f GB each)" % (E * b / 1e9))
                        if flush is None else "L2 flushed before every timed step",
-                       "schedule": {"forward": ["streaming", "fused"][s_f] + (f" K={k_f}" if s_f else ""),
-                                    "backward": ["streaming", "fused"][s_b] + (f" K={k_b}" if s_b else "")},
+                       "schedule": {"forward": SCHEDULES[s_f] + (f" K={k_f}" if s_f == 1 else ""),
+                                    "backward": SCHEDULES[s_b] + (f" K={k_b}" if s_b == 1 else "")},
                        "algorithmic_bytes_per_step": bytes_step_all},
             "pct_of_peak": round(100 * value / peak, 2),
             "elements_per_s": round(E_all / (ms_per_step * 1e-3), 1),

@@ -17,6 +17,22 @@
 
 namespace iabn {
 
+// Block coordinates of a kernel body: the hardware ones, or a virtual block of a
+// persistent (cooperative) kernel that runs several phases in one launch.
+struct Blk {
+    uint32_t x, y, nx, ny;
+};
+__device__ __forceinline__ Blk hw_blk() { return {blockIdx.x, blockIdx.y, gridDim.x, gridDim.y}; }
+
+// Coefficient loads: read-only path (NC) when the coefficients come from an earlier
+// launch; a plain (coherent) load when a cooperative kernel wrote them in this launch
+// (ordered after the writers by the grid barrier's acquire + bar.sync).
+template <bool NC>
+__device__ __forceinline__ float4 ld_coef(const float4* p) {
+    if constexpr (NC) return __ldg(p);
+    else return *p;
+}
+
 #ifndef IABN_STREAM_UNROLL
 #define IABN_STREAM_UNROLL 4
 #endif
@@ -83,13 +99,13 @@ struct PlaneCursor {
 // NCHW: grid (C, S); CTA (c, s) reduces channel-space [lo, hi) of m = N*HW values;
 // channel-space index j lives at x[((j / HW) * C + c) * HW + j % HW].
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads)
-    stats_nchw_kernel(const T* __restrict__ x, int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw,
-                      double* __restrict__ part) {
+__device__ __forceinline__ void stats_nchw_body(const T* __restrict__ x, int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw,
+                      double* __restrict__ part,
+        const Blk bk) {
     constexpr int V = VEC ? Elem<T>::kVec : 1;
     __shared__ double red[2 * kThreads / 32];
-    const int64_t c = blockIdx.x;
-    const int S = gridDim.y, s = blockIdx.y;
+    const int64_t c = bk.x;
+    const int S = bk.ny, s = bk.y;
     const uint32_t mv = m / V;
     const uint32_t vlo = (uint32_t)((uint64_t)mv * s / S), vhi = (uint32_t)((uint64_t)mv * (s + 1) / S);
     const float K = ld_scalar<T>(x + c * HW);
@@ -203,18 +219,25 @@ __global__ void __launch_bounds__(kThreads)
         write_raw_moments(part + ((int64_t)s * C + c) * 3, (double)(vhi - vlo) * V, K, v2[0],
                           v2[1]);
 }
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    stats_nchw_kernel(const T* __restrict__ x, int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw,
+                      double* __restrict__ part) {
+    stats_nchw_body<T, VEC>(x, C, HW, m, fd_hw, part, hw_blk());
+}
+
 
 // NHWC ([rows][C], rows = N*HW): block = 16 (channel groups of V) x 16 (rows);
 // grid (ceil(C / (16 V)), S); CTA reduces rows [rlo, rhi) for 16*V channels.
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads)
-    stats_nhwc_kernel(const T* __restrict__ x, int64_t C, int64_t rows, double* __restrict__ part) {
+__device__ __forceinline__ void stats_nhwc_body(const T* __restrict__ x, int64_t C, int64_t rows, double* __restrict__ part,
+        const Blk bk) {
     constexpr int V = VEC ? Elem<T>::kVec : 1;
     constexpr int CT = 16 * V;
     __shared__ double red[16][CT][2];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int S = gridDim.y, s = blockIdx.y;
-    const int64_t c0 = (int64_t)blockIdx.x * CT + tx * V;
+    const int S = bk.ny, s = bk.y;
+    const int64_t c0 = (int64_t)bk.x * CT + tx * V;
     const int64_t rlo = rows * s / S, rhi = rows * (s + 1) / S;
     const bool active = c0 < C;
     float K[V];
@@ -285,7 +308,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     const int t = threadIdx.x;
     if (t < CT) {
-        const int64_t c = (int64_t)blockIdx.x * CT + t;
+        const int64_t c = (int64_t)bk.x * CT + t;
         if (c < C) {
             double S1 = 0.0, S2 = 0.0;
             for (int y = 0; y < 16; ++y) {
@@ -297,6 +320,12 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
 }
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    stats_nhwc_kernel(const T* __restrict__ x, int64_t C, int64_t rows, double* __restrict__ part) {
+    stats_nhwc_body<T, VEC>(x, C, rows, part, hw_blk());
+}
+
 
 // Sum S partial records of NV doubles per channel in fixed order: out[c][k].
 // extra >= 0: out[NV*C] = extra (the count slot of the backward sums).
@@ -309,6 +338,7 @@ __device__ __forceinline__ void warp_split_sum(const double* __restrict__ part, 
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+#pragma unroll 4
     for (int s = lane; s < S; s += 32)
 #pragma unroll
         for (int k = 0; k < NV; ++k) acc[k] += part[((int64_t)s * C + c) * NV + k];
@@ -371,8 +401,10 @@ __device__ __forceinline__ float4 fwd_coef_from_moments(double cnt, double sum, 
 }
 
 // y = ((x - mu_hi) - mu_lo) A + beta
+// y = (x - mu_hi) A + (beta - mu_lo A): the same operations as the vectorised apply
+// kernels (fwd_apply_rows / fwd_apply_nhwc / fused), so every schedule rounds alike
 __device__ __forceinline__ float affine(float x, const float4& cf) {
-    return fmaf((x - cf.y) - cf.z, cf.x, cf.w);
+    return fmaf(x - cf.y, cf.x, fmaf(-cf.z, cf.x, cf.w));
 }
 
 __device__ __forceinline__ void update_running(float* rm, float* rv, int64_t c, double mean,
@@ -385,9 +417,8 @@ __device__ __forceinline__ void update_running(float* rm, float* rv, int64_t c, 
     }
 }
 
-__global__ void fwd_coef_kernel(FwdCoefArgs a) {
-    const int64_t c = warp_channel();
-    if (c >= a.C) return;
+// warp-level: all 32 lanes of the warp call it for channel c
+__device__ __forceinline__ void fwd_coef_body(const FwdCoefArgs& a, int64_t c) {
     double acc[3];
     warp_split_sum<3>(a.part, a.S, a.C, c, acc);
     if (threadIdx.x & 31) return;
@@ -398,6 +429,10 @@ __global__ void fwd_coef_kernel(FwdCoefArgs a) {
     if (a.save_mean) a.save_mean[c] = (float)mean;
     if (a.save_var) a.save_var[c] = (float)var;
     update_running(a.running_mean, a.running_var, c, mean, var, cnt, a.momentum, a.flags);
+}
+__global__ void fwd_coef_kernel(FwdCoefArgs a) {
+    const int64_t c = warp_channel();
+    if (c < a.C) fwd_coef_body(a, c);
 }
 
 // Eval mode: fixed running statistics.
@@ -431,14 +466,14 @@ __device__ __forceinline__ float leaky(float y, float slope) { return y >= 0.f ?
 // multiple of 16 (a 16-byte vector lies in one channel) or NHWC with C*b a
 // multiple of 16 (a vector holds channels c0 .. c0+V-1); otherwise the channel
 // is resolved per element.
-template <typename T, int LAYOUT, bool ALIGNED>
-__global__ void __launch_bounds__(kThreads)
-    fwd_apply_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
-                     FastDiv fd_c, float slope) {
+template <typename T, int LAYOUT, bool ALIGNED, bool NC = true>
+__device__ __forceinline__ void fwd_apply_body(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
+                     FastDiv fd_c, float slope,
+        const Blk bk) {
     constexpr int V = Elem<T>::kVec;
     const uint32_t nvec = E / V;
-    const uint32_t stride = gridDim.x * kThreads;
-    for (uint32_t base = blockIdx.x * kThreads + threadIdx.x; base < nvec;
+    const uint32_t stride = bk.nx * kThreads;
+    for (uint32_t base = bk.x * kThreads + threadIdx.x; base < nvec;
          base += stride * kUnroll) {
         uint4 r[kUnroll];
 #pragma unroll
@@ -454,17 +489,17 @@ __global__ void __launch_bounds__(kThreads)
                 unpack<T>(r[u], f);
                 const uint32_t e = v * V;
                 if (ALIGNED && LAYOUT == 0) {  // NCHW: the vector lies in one channel
-                    const float4 cf = __ldg(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
+                    const float4 cf = ld_coef<NC>(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
 #pragma unroll
                     for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], cf), slope);
                 } else if (ALIGNED) {  // NHWC, C % V == 0: channels c0 .. c0+V-1
                     const uint32_t c0 = channel_of<LAYOUT>(e, fd_hw, fd_c);
 #pragma unroll
-                    for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], __ldg(coef + c0 + k)), slope);
+                    for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], ld_coef<NC>(coef + c0 + k)), slope);
                 } else {
 #pragma unroll
                     for (int k = 0; k < V; ++k) {
-                        const float4 cf = __ldg(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
+                        const float4 cf = ld_coef<NC>(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
                         f[k] = leaky(affine(f[k], cf), slope);
                     }
                 }
@@ -473,26 +508,33 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
     // tail (E % V elements) by the first threads of block 0
-    if (blockIdx.x == 0 && threadIdx.x < E - nvec * V) {
+    if (bk.x == 0 && threadIdx.x < E - nvec * V) {
         const uint32_t e = nvec * V + threadIdx.x;
         const float4 cf = coef[channel_of<LAYOUT>(e, fd_hw, fd_c)];
         st_scalar<T>(z + e, leaky(affine(ld_scalar<T>(x + e), cf), slope));
     }
 }
+template <typename T, int LAYOUT, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads)
+    fwd_apply_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
+                     FastDiv fd_c, float slope) {
+    fwd_apply_body<T, LAYOUT, ALIGNED>(x, z, coef, E, fd_hw, fd_c, slope, hw_blk());
+}
+
 
 // F2 for NCHW with HW*b a multiple of 16 (the usual case): a grid-stride walk
 // over 16-byte vectors (the whole grid sweeps one contiguous window at a time)
 // with a (plane offset, channel) cursor advanced by the fixed stride -- no
 // divisions in the loop -- and kUnroll loads issued before the math.
 // y = (x - mu_hi) A + (beta - mu_lo A), z = max(y, a y).
-template <typename T>
-__global__ void __launch_bounds__(kThreads)
-    fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
-                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope) {
+template <typename T, bool NC = true>
+__device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
+                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope,
+        const Blk bk) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
-    const uint32_t stride = gridDim.x * kThreads;  // vectors
-    uint32_t v = blockIdx.x * kThreads + threadIdx.x;
+    const uint32_t stride = bk.nx * kThreads;  // vectors
+    uint32_t v = bk.x * kThreads + threadIdx.x;
     if (v >= nvec) return;
     // cursor of element e = v V: plane offset sp, channel c; one stride = q planes + rr
     const uint32_t se = stride * V;
@@ -503,7 +545,7 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t c = row - fdiv(row, fd_c) * C;
     const float2 sl2 = make_float2(slope, slope);
     auto apply = [&](const uint4 r, const uint32_t cc, const uint32_t vv) {
-        const float4 cf = __ldg(coef + cc);  // (A, mu_hi, mu_lo, beta)
+        const float4 cf = ld_coef<NC>(coef + cc);  // (A, mu_hi, mu_lo, beta)
         const float bp = fmaf(-cf.z, cf.x, cf.w);
         const float2 A2 = make_float2(cf.x, cf.x), B2 = make_float2(bp, bp);
         float2 w[NP];
@@ -544,6 +586,13 @@ __global__ void __launch_bounds__(kThreads)
         apply(r, cc, vv);
     }
 }
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
+                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope) {
+    fwd_apply_rows_body<T>(x, z, coef, nvec, HW, C, fd_hw, fd_c, slope, hw_blk());
+}
+
 
 // ====================================================================== B1: gradient sums
 // Per element (Alg. 2 l.2-5): dy = f'(z) dz, y = f^-1(z),
@@ -565,16 +614,16 @@ __device__ __forceinline__ void grad_terms(float z, float dz, float slope, float
 }
 
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads)
-    bwd_reduce_nchw_kernel(const T* __restrict__ z, const T* __restrict__ dz,
+__device__ __forceinline__ void bwd_reduce_nchw_body(const T* __restrict__ z, const T* __restrict__ dz,
                            const float* __restrict__ gamma, const float* __restrict__ beta,
                            int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw, float eps,
                            float slope, float inv_slope, uint32_t flags,
-                           double* __restrict__ part) {
+                           double* __restrict__ part,
+        const Blk bk) {
     constexpr int V = VEC ? Elem<T>::kVec : 1;
     __shared__ double red[2 * kThreads / 32];
-    const int64_t c = blockIdx.x;
-    const int S = gridDim.y, s = blockIdx.y;
+    const int64_t c = bk.x;
+    const int S = bk.ny, s = bk.y;
     const uint32_t mv = m / V;
     const uint32_t vlo = (uint32_t)((uint64_t)mv * s / S), vhi = (uint32_t)((uint64_t)mv * (s + 1) / S);
     const InvAffine ia = inv_affine(gamma[c], beta[c], eps, flags);
@@ -685,19 +734,29 @@ __global__ void __launch_bounds__(kThreads)
         o[1] = v2[1];
     }
 }
-
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kThreads)
-    bwd_reduce_nhwc_kernel(const T* __restrict__ z, const T* __restrict__ dz,
+    bwd_reduce_nchw_kernel(const T* __restrict__ z, const T* __restrict__ dz,
+                           const float* __restrict__ gamma, const float* __restrict__ beta,
+                           int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw, float eps,
+                           float slope, float inv_slope, uint32_t flags,
+                           double* __restrict__ part) {
+    bwd_reduce_nchw_body<T, VEC>(z, dz, gamma, beta, C, HW, m, fd_hw, eps, slope, inv_slope, flags, part, hw_blk());
+}
+
+
+template <typename T, bool VEC>
+__device__ __forceinline__ void bwd_reduce_nhwc_body(const T* __restrict__ z, const T* __restrict__ dz,
                            const float* __restrict__ gamma, const float* __restrict__ beta,
                            int64_t C, int64_t rows, float eps, float slope, float inv_slope,
-                           uint32_t flags, double* __restrict__ part) {
+                           uint32_t flags, double* __restrict__ part,
+        const Blk bk) {
     constexpr int V = VEC ? Elem<T>::kVec : 1;
     constexpr int CT = 16 * V;
     __shared__ double red[16][CT][2];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int S = gridDim.y, s = blockIdx.y;
-    const int64_t c0 = (int64_t)blockIdx.x * CT + tx * V;
+    const int S = bk.ny, s = bk.y;
+    const int64_t c0 = (int64_t)bk.x * CT + tx * V;
     const int64_t rlo = rows * s / S, rhi = rows * (s + 1) / S;
     const bool active = c0 < C;
     InvAffine ia[V];
@@ -761,7 +820,7 @@ __global__ void __launch_bounds__(kThreads)
     __syncthreads();
     const int t = threadIdx.x;
     if (t < CT) {
-        const int64_t c = (int64_t)blockIdx.x * CT + t;
+        const int64_t c = (int64_t)bk.x * CT + t;
         if (c < C) {
             double S1 = 0.0, S2 = 0.0;
             for (int y = 0; y < 16; ++y) {
@@ -774,6 +833,15 @@ __global__ void __launch_bounds__(kThreads)
         }
     }
 }
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kThreads)
+    bwd_reduce_nhwc_kernel(const T* __restrict__ z, const T* __restrict__ dz,
+                           const float* __restrict__ gamma, const float* __restrict__ beta,
+                           int64_t C, int64_t rows, float eps, float slope, float inv_slope,
+                           uint32_t flags, double* __restrict__ part) {
+    bwd_reduce_nhwc_body<T, VEC>(z, dz, gamma, beta, C, rows, eps, slope, inv_slope, flags, part, hw_blk());
+}
+
 
 // B2 coefficients (refolded in y):
 //   dx = g rstd (dy - x^ S2/m - S1/m),  x^ = (y - beta)/g
@@ -809,9 +877,8 @@ __device__ __forceinline__ float4 bwd_coef_from_sums(double S1, double S2, doubl
     return make_float4((float)alpha, (float)kappa, (float)cc, 0.f);
 }
 
-__global__ void bwd_coef_kernel(BwdCoefArgs a) {
-    const int64_t c = warp_channel();
-    if (c >= a.C) return;
+// warp-level: all 32 lanes of the warp call it for channel c
+__device__ __forceinline__ void bwd_coef_body(const BwdCoefArgs& a, int64_t c) {
     double gs[2], ls[2];
     warp_split_sum<2>(a.glob, a.S_glob, a.C, c, gs);
     if (a.loc == a.glob) {
@@ -827,16 +894,20 @@ __global__ void bwd_coef_kernel(BwdCoefArgs a) {
     a.dbeta[c] = (float)l1;
     a.dgamma[c] = (float)(gamma_sign(a.gamma[c], a.flags) * l2);
 }
+__global__ void bwd_coef_kernel(BwdCoefArgs a) {
+    const int64_t c = warp_channel();
+    if (c < a.C) bwd_coef_body(a, c);
+}
 
 // B2: dx = alpha dy + kappa y + cc, dx may alias dz.
-template <typename T, int LAYOUT, bool ALIGNED>
-__global__ void __launch_bounds__(kThreads)
-    bwd_apply_kernel(const T* __restrict__ z, const T* dz, T* dx, const float4* __restrict__ coef,
-                     uint32_t E, FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope) {
+template <typename T, int LAYOUT, bool ALIGNED, bool NC = true>
+__device__ __forceinline__ void bwd_apply_body(const T* __restrict__ z, const T* dz, T* dx, const float4* __restrict__ coef,
+                     uint32_t E, FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope,
+        const Blk bk) {
     constexpr int V = Elem<T>::kVec;
     const uint32_t nvec = E / V;
-    const uint32_t stride = gridDim.x * kThreads;
-    for (uint32_t base = blockIdx.x * kThreads + threadIdx.x; base < nvec;
+    const uint32_t stride = bk.nx * kThreads;
+    for (uint32_t base = bk.x * kThreads + threadIdx.x; base < nvec;
          base += stride * kUnroll) {
         uint4 rz[kUnroll], rd[kUnroll];
 #pragma unroll
@@ -858,11 +929,11 @@ __global__ void __launch_bounds__(kThreads)
                 float4 cf;
                 uint32_t c0 = 0;
                 if (ALIGNED) c0 = channel_of<LAYOUT>(e, fd_hw, fd_c);
-                if (ALIGNED && LAYOUT == 0) cf = __ldg(coef + c0);  // NCHW: one channel
+                if (ALIGNED && LAYOUT == 0) cf = ld_coef<NC>(coef + c0);  // NCHW: one channel
 #pragma unroll
                 for (int k = 0; k < V; ++k) {
-                    if (ALIGNED && LAYOUT == 1) cf = __ldg(coef + c0 + k);  // NHWC: c0 + k
-                    if (!ALIGNED) cf = __ldg(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
+                    if (ALIGNED && LAYOUT == 1) cf = ld_coef<NC>(coef + c0 + k);  // NHWC: c0 + k
+                    if (!ALIGNED) cf = ld_coef<NC>(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
                     const bool pos = fz[k] >= 0.f;
                     const float y = pos ? fz[k] : fz[k] * inv_slope;
                     const float dy = pos ? fd[k] : fd[k] * slope;
@@ -872,7 +943,7 @@ __global__ void __launch_bounds__(kThreads)
             }
         }
     }
-    if (blockIdx.x == 0 && threadIdx.x < E - nvec * V) {
+    if (bk.x == 0 && threadIdx.x < E - nvec * V) {
         const uint32_t e = nvec * V + threadIdx.x;
         const float4 cf = coef[channel_of<LAYOUT>(e, fd_hw, fd_c)];
         const float zz = ld_scalar<T>(z + e), dd = ld_scalar<T>(dz + e);
@@ -882,6 +953,13 @@ __global__ void __launch_bounds__(kThreads)
         st_scalar<T>(dx + e, fmaf(cf.x, dy, fmaf(cf.y, y, cf.z)));
     }
 }
+template <typename T, int LAYOUT, bool ALIGNED>
+__global__ void __launch_bounds__(kThreads)
+    bwd_apply_kernel(const T* __restrict__ z, const T* dz, T* dx, const float4* __restrict__ coef,
+                     uint32_t E, FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope) {
+    bwd_apply_body<T, LAYOUT, ALIGNED>(z, dz, dx, coef, E, fd_hw, fd_c, slope, inv_slope, hw_blk());
+}
+
 
 // ====================================================================== NHWC elementwise passes
 // NHWC with C*b a multiple of 16: vector v holds channels (v mod C/V)*V .. +V-1.  The

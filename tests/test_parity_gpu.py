@@ -307,3 +307,37 @@ def test_fold_conv(gamma_mode, with_bias, orc):
     assert wo.data_ptr() == wi.data_ptr()
     assert torch.equal(wo.cpu(), torch.from_numpy(w2).float())
     assert torch.equal(bo.cpu(), torch.from_numpy(b2).float())
+
+
+# ------------------------------------------------------------------ one-launch (cooperative) schedule
+ONE = 1 << 10
+COOP_CASES = [
+    Case(8, 40, 196, dtype="f32", seed=20),                    # NCHW aligned
+    Case(8, 40, 196, dtype="bf16", seed=21),                   # NCHW, plane not 16-byte aligned
+    Case(4, 24, 49, dtype="bf16", seed=22),                    # odd plane
+    Case(6, 64, 49, dtype="bf16", layout="NHWC", seed=23),     # NHWC aligned
+    Case(5, 37, 30, dtype="f32", layout="NHWC", seed=24),      # NHWC ragged channels
+    Case(3, 300, 7, dtype="f32", seed=25),                     # many channels, tiny planes
+]
+
+
+@pytest.mark.parametrize("case", COOP_CASES, ids=lambda c: f"{c.layout}_{c.dtype}_{c.N}x{c.C}x{c.HW}")
+def test_coop_parity(case):
+    _check(case, ONE)
+
+
+@pytest.mark.parametrize("case", COOP_CASES[:4], ids=lambda c: f"{c.layout}_{c.dtype}_{c.N}x{c.C}x{c.HW}")
+def test_coop_matches_streaming_bitwise(case):
+    """The one-launch kernel runs the streaming phases with the same partitions."""
+    x, dz, p = inputs(case)
+    a = run_gpu(case, x, dz, p, flags=ONE)
+    b = run_gpu(case, x, dz, p, flags=STREAM)
+    for k in ("z", "mean", "var", "rm", "rv", "dx", "dgamma", "dbeta"):
+        assert torch.equal(a[k], b[k]), k
+
+
+def test_coop_schedule_query():
+    from paper_1712_02616_b200 import _lib as L
+    d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: no TMA, small layer
+    assert L.query_schedule(d, 0)[0] == 0  # opt-in only (measured slower)
+    assert L.query_schedule(d, 0, ONE)[0] == 2 and L.query_schedule(d, 1, ONE)[0] == 2
