@@ -485,6 +485,9 @@ iabn_status launch_coop(const Geom& g, CoopArgs a, cudaStream_t st, int sms) {
                : launch_coop_t<T, 1, false, PASS>(g, a, st, sms);
 }
 
+// covering vectors per plane of the misaligned NCHW reductions (nchw_cover_body)
+FastDiv cover_fd(const Geom& g) { return make_fastdiv((uint32_t)(g.HW / (16 / g.b) + 2)); }
+
 // ====================================================================== streaming launches
 template <typename T>
 iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cudaStream_t st) {
@@ -495,9 +498,10 @@ iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cuda
         if (vec)
             stats_nchw_kernel<T, true><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.HW,
                                                                   (uint32_t)g.m, fd, part);
-        else
-            stats_nchw_kernel<T, false><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.HW,
-                                                                   (uint32_t)g.m, fd, part);
+        else  // planes not 16-byte aligned: masked covering vectors
+            nchw_cover_kernel<T, 0><<<grid, kThreads, 0, st>>>(
+                (const T*)x, nullptr, nullptr, nullptr, g.C, g.HW, g.N, g.E, 0.f, 1.f, 1.f, 0u,
+                cover_fd(g), part);
     } else {
         const int V = vec ? 16 / g.b : 1;
         const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
@@ -522,10 +526,10 @@ iabn_status launch_bwd_reduce(const Geom& g, int S, const void* z, const void* d
             bwd_reduce_nchw_kernel<T, true><<<grid, kThreads, 0, st>>>(
                 (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, (uint32_t)g.m, fd, eps, slope,
                 inv_slope, flags, part);
-        else
-            bwd_reduce_nchw_kernel<T, false><<<grid, kThreads, 0, st>>>(
-                (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, (uint32_t)g.m, fd, eps, slope,
-                inv_slope, flags, part);
+        else  // planes not 16-byte aligned: masked covering vectors
+            nchw_cover_kernel<T, 1><<<grid, kThreads, 0, st>>>(
+                (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, g.N, g.E, eps, slope,
+                inv_slope, flags, cover_fd(g), part);
     } else {
         const int V = vec ? 16 / g.b : 1;
         const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
@@ -583,9 +587,9 @@ iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4
         const T* xp = (const T*)x + off;
         T* zp = (T*)z + off;
         const int grid = apply_grid(E, g.b, sms);
-        if (g.layout == IABN_NCHW && al) {
+        if (g.layout == IABN_NCHW && g.HW >= 16 / g.b) {  // any alignment (straddles handled)
             fwd_apply_rows_kernel<T><<<grid, kThreads, 0, st>>>(
-                xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)g.HW, (uint32_t)g.C, fh, fc, slope);
+                xp, zp, coef, E, (uint32_t)g.HW, (uint32_t)g.C, fh, fc, slope);
         } else if (g.layout == IABN_NCHW) {
             if (al)
                 fwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
@@ -621,7 +625,10 @@ iabn_status launch_bwd_apply(const Geom& g, const void* z, const void* dz, void*
         const T* dzp = (const T*)dz + off;
         T* dxp = (T*)dx + off;
         const int grid = apply_grid(E, g.b, sms);
-        if (g.layout == IABN_NCHW) {
+        if (g.layout == IABN_NCHW && g.HW >= 16 / g.b) {  // any alignment (straddles handled)
+            bwd_apply_rows_kernel<T><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, (uint32_t)g.HW,
+                                                               (uint32_t)g.C, fh, fc, slope, inv_slope);
+        } else if (g.layout == IABN_NCHW) {
             if (al)
                 bwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
             else
@@ -828,6 +835,8 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         a.E = (uint32_t)c.g.E;
         a.fd_hw = fd32(c.g.HW);
         a.fd_c = fd32(c.g.C);
+        a.fd_cover = cover_fd(c.g);
+        a.N = c.g.N;
         a.S = c.S;
         a.part = wsp<double>(c, c.w.part);
         a.coef = wsp<float4>(c, c.w.coef);
@@ -900,6 +909,8 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
         a.E = (uint32_t)c.g.E;
         a.fd_hw = fd32(c.g.HW);
         a.fd_c = fd32(c.g.C);
+        a.fd_cover = cover_fd(c.g);
+        a.N = c.g.N;
         a.S = c.S;
         a.part = part;
         a.coef = wsp<float4>(c, c.w.coef);

@@ -37,9 +37,9 @@ struct CoopArgs {
     const void* in0;  // x (fwd) / z (bwd)
     const void* in1;  // dz (bwd)
     void* out;        // z (fwd) / dx (bwd)
-    int64_t C, HW, rows;
+    int64_t C, HW, rows, N;
     uint32_t m, E;
-    FastDiv fd_hw, fd_c;
+    FastDiv fd_hw, fd_c, fd_cover;
     int S;
     double* part;
     float4* coef;
@@ -61,7 +61,10 @@ __global__ void __launch_bounds__(kThreads, 2) coop_kernel(const CoopArgs a) {
     if (LAYOUT == 0) {
         for (uint32_t vb = blockIdx.x; vb < C * S; vb += gridDim.x) {
             const Blk bk{vb % C, vb / C, C, S};
-            if (PASS == 0)
+            if (!VEC)  // planes not 16-byte aligned: masked covering vectors
+                nchw_cover_body<T, PASS>(in0, in1, a.gamma, a.beta, a.C, a.HW, a.N, a.E, a.eps,
+                                         a.slope, a.inv_slope, a.flags, a.fd_cover, a.part, bk);
+            else if (PASS == 0)
                 stats_nchw_body<T, VEC>(in0, a.C, a.HW, a.m, a.fd_hw, a.part, bk);
             else
                 bwd_reduce_nchw_body<T, VEC>(in0, in1, a.gamma, a.beta, a.C, a.HW, a.m, a.fd_hw,
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 2) coop_kernel(const CoopArgs a) {
     // ---- phase 3: elementwise apply (inputs re-read from L2)
     const Blk bk{blockIdx.x, 0, gridDim.x, 1};
     if (PASS == 0 && LAYOUT == 0 && VEC)
-        fwd_apply_rows_body<T, false>(in0, (T*)a.out, a.coef, a.E / Elem<T>::kVec, (uint32_t)a.HW, C,
+        fwd_apply_rows_body<T, false>(in0, (T*)a.out, a.coef, a.E, (uint32_t)a.HW, C,
                                a.fd_hw, a.fd_c, a.slope, bk);
     else if (PASS == 0)
         fwd_apply_body<T, LAYOUT, VEC, false>(in0, (T*)a.out, a.coef, a.E, a.fd_hw, a.fd_c,

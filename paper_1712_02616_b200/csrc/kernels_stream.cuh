@@ -522,19 +522,27 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 
-// F2 for NCHW with HW*b a multiple of 16 (the usual case): a grid-stride walk
-// over 16-byte vectors (the whole grid sweeps one contiguous window at a time)
-// with a (plane offset, channel) cursor advanced by the fixed stride -- no
-// divisions in the loop -- and kUnroll loads issued before the math.
+// F2 for NCHW with HW >= V (any alignment): a grid-stride walk over 16-byte vectors
+// (the whole grid sweeps one contiguous window at a time) with a (plane offset,
+// channel) cursor advanced by the fixed stride -- no divisions in the loop -- and
+// kUnroll loads issued before the math.  A vector that straddles two planes (HW*b
+// not a multiple of 16) takes its tail elements' coefficients from the next channel.
 // y = (x - mu_hi) A + (beta - mu_lo A), z = max(y, a y).
 template <typename T, bool NC = true>
-__device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
-                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope,
-        const Blk bk) {
+__device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const float4* __restrict__ coef,
+                                                    uint32_t E, uint32_t HW, uint32_t C,
+                                                    FastDiv fd_hw, FastDiv fd_c, float slope,
+                                                    const Blk bk) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
+    const uint32_t nvec = E / V;
     const uint32_t stride = bk.nx * kThreads;  // vectors
     uint32_t v = bk.x * kThreads + threadIdx.x;
+    if (bk.x == 0 && threadIdx.x < E - nvec * V) {  // tail elements
+        const uint32_t e = nvec * V + threadIdx.x;
+        const float4 cf = ld_coef<NC>(coef + channel_of<0>(e, fd_hw, fd_c));
+        st_scalar<T>(z + e, leaky(affine(ld_scalar<T>(x + e), cf), slope));
+    }
     if (v >= nvec) return;
     // cursor of element e = v V: plane offset sp, channel c; one stride = q planes + rr
     const uint32_t se = stride * V;
@@ -544,19 +552,35 @@ __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const floa
     uint32_t sp = v * V - row * HW;
     uint32_t c = row - fdiv(row, fd_c) * C;
     const float2 sl2 = make_float2(slope, slope);
-    auto apply = [&](const uint4 r, const uint32_t cc, const uint32_t vv) {
+    auto apply = [&](const uint4 r, const uint32_t cc, const uint32_t spv, const uint32_t vv) {
         const float4 cf = ld_coef<NC>(coef + cc);  // (A, mu_hi, mu_lo, beta)
         const float bp = fmaf(-cf.z, cf.x, cf.w);
-        const float2 A2 = make_float2(cf.x, cf.x), B2 = make_float2(bp, bp);
-        float2 w[NP];
-        Pairs<T>::load_sub(r, cf.y, w);
+        if (spv + V <= HW) {
+            const float2 A2 = make_float2(cf.x, cf.x), B2 = make_float2(bp, bp);
+            float2 w[NP];
+            Pairs<T>::load_sub(r, cf.y, w);
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-            const float2 y = fma2(w[i], A2, B2);
-            const float2 ay = mul2(y, sl2);
-            w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+            for (int i = 0; i < NP; ++i) {
+                const float2 y = fma2(w[i], A2, B2);
+                const float2 ay = mul2(y, sl2);
+                w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+            }
+            st_vec(z + (size_t)vv * V, Pairs<T>::store(w));
+        } else {  // elements k >= HW - spv belong to the next channel
+            const float4 cf2 = ld_coef<NC>(coef + (cc + 1 == C ? 0 : cc + 1));
+            const float bp2 = fmaf(-cf2.z, cf2.x, cf2.w);
+            const uint32_t kb = HW - spv;
+            float f[V];
+            unpack<T>(r, f);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const bool first = (uint32_t)k < kb;
+                const float y = fmaf(f[k] - (first ? cf.y : cf2.y), first ? cf.x : cf2.x,
+                                     first ? bp : bp2);
+                f[k] = fmaxf(y, y * slope);
+            }
+            st_vec(z + (size_t)vv * V, pack<T>(f));
         }
-        st_vec(z + (size_t)vv * V, Pairs<T>::store(w));
     };
     auto advance = [&]() {
         v += stride;
@@ -568,31 +592,31 @@ __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const floa
     };
     for (; v + (kUnroll - 1) * stride < nvec;) {
         uint4 r[kUnroll];
-        uint32_t cu[kUnroll], vu[kUnroll];
+        uint32_t cu[kUnroll], su[kUnroll], vu[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             r[u] = ld_vec(x + (size_t)v * V);
             cu[u] = c;
+            su[u] = sp;
             vu[u] = v;
             advance();
         }
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) apply(r[u], cu[u], vu[u]);
+        for (int u = 0; u < kUnroll; ++u) apply(r[u], cu[u], su[u], vu[u]);
     }
     for (; v < nvec;) {
         const uint4 r = ld_vec(x + (size_t)v * V);
-        const uint32_t cc = c, vv = v;
+        const uint32_t cc = c, ss = sp, vv = v;
         advance();
-        apply(r, cc, vv);
+        apply(r, cc, ss, vv);
     }
 }
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
-    fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
+    fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E,
                           uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope) {
-    fwd_apply_rows_body<T>(x, z, coef, nvec, HW, C, fd_hw, fd_c, slope, hw_blk());
+    fwd_apply_rows_body<T>(x, z, coef, E, HW, C, fd_hw, fd_c, slope, hw_blk());
 }
-
 
 // ====================================================================== B1: gradient sums
 // Per element (Alg. 2 l.2-5): dy = f'(z) dz, y = f^-1(z),
@@ -960,6 +984,203 @@ __global__ void __launch_bounds__(kThreads)
     bwd_apply_body<T, LAYOUT, ALIGNED>(z, dz, dx, coef, E, fd_hw, fd_c, slope, inv_slope, hw_blk());
 }
 
+
+// B2 for NCHW with HW >= V (any alignment): the stride cursor of fwd_apply_rows_body;
+// dx = al dy + ka y + cc with (al, ka, cc) of the element's channel.
+template <typename T, bool NC = true>
+__device__ __forceinline__ void bwd_apply_rows_body(const T* __restrict__ z, const T* dz, T* dx,
+                                                    const float4* __restrict__ coef, uint32_t E,
+                                                    uint32_t HW, uint32_t C, FastDiv fd_hw,
+                                                    FastDiv fd_c, float slope, float inv_slope,
+                                                    const Blk bk) {
+    constexpr int V = Elem<T>::kVec;
+    const uint32_t nvec = E / V;
+    const uint32_t stride = bk.nx * kThreads;
+    uint32_t v = bk.x * kThreads + threadIdx.x;
+    auto grad = [&](float zz, float dd, const float4& cf) {
+        const bool pos = zz >= 0.f;  // -0.0 counts as >= 0
+        const float y = pos ? zz : zz * inv_slope;
+        const float dy = pos ? dd : dd * slope;
+        return fmaf(cf.x, dy, fmaf(cf.y, y, cf.z));
+    };
+    if (bk.x == 0 && threadIdx.x < E - nvec * V) {  // tail elements
+        const uint32_t e = nvec * V + threadIdx.x;
+        const float4 cf = ld_coef<NC>(coef + channel_of<0>(e, fd_hw, fd_c));
+        st_scalar<T>(dx + e, grad(ld_scalar<T>(z + e), ld_scalar<T>(dz + e), cf));
+    }
+    if (v >= nvec) return;
+    const uint32_t se = stride * V;
+    const uint32_t q = fdiv(se, fd_hw), rr = se - q * HW;
+    const uint32_t qc = q - fdiv(q, fd_c) * C;
+    uint32_t row = fdiv(v * V, fd_hw);
+    uint32_t sp = v * V - row * HW;
+    uint32_t c = row - fdiv(row, fd_c) * C;
+    auto apply = [&](const uint4 rz, const uint4 rd, const uint32_t cc, const uint32_t spv,
+                     const uint32_t vv) {
+        const float4 cf = ld_coef<NC>(coef + cc);
+        const float4 cf2 = spv + V <= HW ? cf : ld_coef<NC>(coef + (cc + 1 == C ? 0 : cc + 1));
+        const uint32_t kb = HW - spv;  // elements k >= kb belong to the next channel
+        float fz[V], fd[V];
+        unpack<T>(rz, fz);
+        unpack<T>(rd, fd);
+#pragma unroll
+        for (int k = 0; k < V; ++k) fz[k] = grad(fz[k], fd[k], (uint32_t)k < kb ? cf : cf2);
+        st_vec(dx + (size_t)vv * V, pack<T>(fz));
+    };
+    auto advance = [&]() {
+        v += stride;
+        sp += rr;
+        const bool carry = sp >= HW;
+        sp = carry ? sp - HW : sp;
+        c += qc + (carry ? 1u : 0u);
+        c = c >= C ? c - C : c;
+    };
+    for (; v + (kUnroll - 1) * stride < nvec;) {
+        uint4 rz[kUnroll], rd[kUnroll];
+        uint32_t cu[kUnroll], su[kUnroll], vu[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            rz[u] = ld_vec(z + (size_t)v * V);
+            rd[u] = ld_vec(dz + (size_t)v * V);
+            cu[u] = c;
+            su[u] = sp;
+            vu[u] = v;
+            advance();
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) apply(rz[u], rd[u], cu[u], su[u], vu[u]);
+    }
+    for (; v < nvec;) {
+        const uint4 rz = ld_vec(z + (size_t)v * V), rd = ld_vec(dz + (size_t)v * V);
+        const uint32_t cc = c, ss = sp, vv = v;
+        advance();
+        apply(rz, rd, cc, ss, vv);
+    }
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads)
+    bwd_apply_rows_kernel(const T* __restrict__ z, const T* dz, T* dx,
+                          const float4* __restrict__ coef, uint32_t E, uint32_t HW, uint32_t C,
+                          FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope) {
+    bwd_apply_rows_body<T>(z, dz, dx, coef, E, HW, C, fd_hw, fd_c, slope, inv_slope, hw_blk());
+}
+
+// ====================================================================== misaligned NCHW reductions
+// NCHW with HW*b not a multiple of 16 (e.g. bf16 14x14: 392-byte planes): plane n of
+// channel c starts at element P = (n C + c) HW, not on a 16-byte boundary.  Each plane
+// is read as the aligned 16-byte vectors that cover it (at most W = HW/V + 2), the
+// elements outside [P, P + HW) masked out -- full-width loads, a few neighbour bytes
+// per plane (served by L2).  Work item u = n W + i: vector i of plane n; split s of S
+// takes items [N W s / S, N W (s+1) / S).  PASS 0: raw moments (count, sum, sum of
+// squares) shifted by K; PASS 1: (sum dy, sum dy x^) as bwd_reduce_nchw_body.
+template <typename T, int PASS>
+__device__ __forceinline__ void nchw_cover_body(const T* __restrict__ in0, const T* __restrict__ in1,
+                                                const float* __restrict__ gamma,
+                                                const float* __restrict__ beta, int64_t C,
+                                                int64_t HW, int64_t N, int64_t E, float eps,
+                                                float slope, float inv_slope, uint32_t flags,
+                                                FastDiv fdw, double* __restrict__ part,
+                                                const Blk bk) {
+    constexpr int V = Elem<T>::kVec;
+    __shared__ double red[3 * kThreads / 32];
+    const int64_t c = bk.x;
+    const int S = bk.ny, s = bk.y;
+    const uint32_t W = fdw.d;  // HW / V + 2 covering vectors per plane
+    const uint64_t items = (uint64_t)N * W;
+    const uint32_t ulo = (uint32_t)(items * s / S), uhi = (uint32_t)(items * (s + 1) / S);
+    const float K = PASS == 0 ? ld_scalar<T>(in0 + c * HW) : 0.f;
+    InvAffine ia{0.f, 0.f};
+    if (PASS == 1) ia = inv_affine(gamma[c], beta[c], eps, flags);
+    float a1[V], a2[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
+    double d1 = 0.0, d2 = 0.0;
+    uint32_t cnt = 0;
+    int iter = 0;
+    for (uint32_t u0 = ulo + threadIdx.x; u0 < uhi; u0 += kThreads * kUnroll) {
+        uint4 r0[kUnroll], r1[kUnroll];
+        int64_t e0[kUnroll], p0[kUnroll];
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+            const uint32_t u = u0 + q * kThreads;
+            const uint32_t n = fdiv(u, fdw), i = u - n * W;
+            const int64_t P = ((int64_t)n * C + c) * HW;
+            const int64_t ev = (P / V + i) * V;  // first element of the covering vector
+            p0[q] = P;
+            e0[q] = (u < uhi && ev < P + HW) ? ev : -1;
+            if (e0[q] >= 0 && ev + V <= E) {
+                r0[q] = ld_vec_ro(in0 + ev);
+                if (PASS == 1) r1[q] = ld_vec_ro(in1 + ev);
+            } else if (e0[q] >= 0) {  // the tensor's last, partial vector
+                float f0[V], f1[V];
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    f0[k] = ev + k < E ? ld_scalar<T>(in0 + ev + k) : 0.f;
+                    f1[k] = (PASS == 1 && ev + k < E) ? ld_scalar<T>(in1 + ev + k) : 0.f;
+                }
+                r0[q] = pack<T>(f0);
+                r1[q] = pack<T>(f1);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kUnroll; ++q) {
+            if (e0[q] < 0) continue;
+            float f0[V], f1[V];
+            unpack<T>(r0[q], f0);
+            if (PASS == 1) unpack<T>(r1[q], f1);
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                const int64_t e = e0[q] + k;
+                const bool in = e >= p0[q] && e < p0[q] + HW;
+                if (PASS == 0) {
+                    const float d = in ? f0[k] - K : 0.f;
+                    a1[k] += d;
+                    a2[k] = fmaf(d, d, a2[k]);
+                    cnt += in ? 1u : 0u;
+                } else {
+                    float dy, xh;
+                    grad_terms(f0[k], in ? f1[k] : 0.f, slope, inv_slope, ia, dy, xh);
+                    a1[k] += dy;
+                    a2[k] = fmaf(dy, xh, a2[k]);
+                }
+            }
+        }
+        if (++iter == 16) {
+            iter = 0;
+#pragma unroll
+            for (int k = 0; k < V; ++k) {
+                d1 += a1[k];
+                d2 += a2[k];
+                a1[k] = a2[k] = 0.f;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        d1 += a1[k];
+        d2 += a2[k];
+    }
+    double v3[3] = {d1, d2, (double)cnt};
+    block_sum<3>(v3, red);
+    if (threadIdx.x == 0) {
+        if (PASS == 0) {
+            write_raw_moments(part + ((int64_t)s * C + c) * 3, v3[2], K, v3[0], v3[1]);
+        } else {
+            double* o = part + ((int64_t)s * C + c) * 2;
+            o[0] = v3[0];
+            o[1] = v3[1];
+        }
+    }
+}
+template <typename T, int PASS>
+__global__ void __launch_bounds__(kThreads)
+    nchw_cover_kernel(const T* __restrict__ in0, const T* __restrict__ in1,
+                      const float* __restrict__ gamma, const float* __restrict__ beta, int64_t C,
+                      int64_t HW, int64_t N, int64_t E, float eps, float slope, float inv_slope,
+                      uint32_t flags, FastDiv fdw, double* __restrict__ part) {
+    nchw_cover_body<T, PASS>(in0, in1, gamma, beta, C, HW, N, E, eps, slope, inv_slope, flags,
+                             fdw, part, hw_blk());
+}
 
 // ====================================================================== NHWC elementwise passes
 // NHWC with C*b a multiple of 16: vector v holds channels (v mod C/V)*V .. +V-1.  The
