@@ -82,10 +82,14 @@ iabn_status device_facts(DevFacts** out) {
     }
     if (!f.attrs_set) {
         const int dyn = f.max_smem_optin - 4096;  // leave room for static smem
-        const void* fns[] = {(const void*)fused_kernel<float, 0>,
-                             (const void*)fused_kernel<__nv_bfloat16, 0>,
-                             (const void*)fused_kernel<float, 1>,
-                             (const void*)fused_kernel<__nv_bfloat16, 1>};
+        const void* fns[] = {(const void*)fused_kernel<float, 0, 2>,
+                             (const void*)fused_kernel<__nv_bfloat16, 0, 2>,
+                             (const void*)fused_kernel<float, 1, 2>,
+                             (const void*)fused_kernel<__nv_bfloat16, 1, 2>,
+                             (const void*)fused_kernel<float, 0, 4>,
+                             (const void*)fused_kernel<__nv_bfloat16, 0, 4>,
+                             (const void*)fused_kernel<float, 1, 4>,
+                             (const void*)fused_kernel<__nv_bfloat16, 1, 4>};
         for (const void* fn : fns) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -254,23 +258,31 @@ struct FusedPlan {
     uint32_t chunk_vecs = 0;
     int nbuf = 0;
     size_t smem = 0;
+    int minb = 2;        // kernel variant: CTAs per SM its registers allow (2 or 4)
 };
 
-const void* fused_fn(int pass, int dtype) {
+const void* fused_fn(int pass, int dtype, int minb) {
+    if (minb == 4) {
+        if (pass == 0)
+            return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0, 4>
+                                     : (const void*)fused_kernel<__nv_bfloat16, 0, 4>;
+        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1, 4>
+                                 : (const void*)fused_kernel<__nv_bfloat16, 1, 4>;
+    }
     if (pass == 0)
-        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0>
-                                 : (const void*)fused_kernel<__nv_bfloat16, 0>;
-    return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1>
-                             : (const void*)fused_kernel<__nv_bfloat16, 1>;
+        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0, 2>
+                                 : (const void*)fused_kernel<__nv_bfloat16, 0, 2>;
+    return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1, 2>
+                             : (const void*)fused_kernel<__nv_bfloat16, 1, 2>;
 }
 
 // Co-resident clusters of K CTAs with `smem` bytes of dynamic shared memory (cached).
-int max_active_clusters(int pass, int dtype, int K, size_t smem) {
+int max_active_clusters(int pass, int dtype, int K, size_t smem, int minb) {
     static std::mutex mu;
     struct Key {
         int dev, pass, dtype, K;
         size_t smem;
-        int val;
+        int minb, val;
     };
     static Key cache[512];
     static int ncache = 0;
@@ -279,7 +291,7 @@ int max_active_clusters(int pass, int dtype, int K, size_t smem) {
     std::lock_guard<std::mutex> lk(mu);
     for (int i = 0; i < ncache; ++i)
         if (cache[i].dev == dev && cache[i].pass == pass && cache[i].dtype == dtype &&
-            cache[i].K == K && cache[i].smem == smem)
+            cache[i].K == K && cache[i].smem == smem && cache[i].minb == minb)
             return cache[i].val;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)K, 1, 1);
@@ -293,11 +305,11 @@ int max_active_clusters(int pass, int dtype, int K, size_t smem) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, fused_fn(pass, dtype), &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, fused_fn(pass, dtype, minb), &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = 0;
     }
-    if (ncache < 512) cache[ncache++] = Key{dev, pass, dtype, K, smem, n};
+    if (ncache < 512) cache[ncache++] = Key{dev, pass, dtype, K, smem, minb, n};
     return n;
 }
 
@@ -319,15 +331,18 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
     const int nforce = env_int("IABN_FUSED_NBUF", 0);
     const int64_t pv = g.HW * g.b / 16;  // vectors per plane
     const int64_t np = g.N;
+    int minb = 2;
+    size_t lim = budget;
     auto consider = [&](int K, int nbuf) -> bool {
         // slice: whole planes when N >= K (see cta_slice)
         const bool by_plane = np >= K;
         const int64_t cap = by_plane ? pv * ((np + K - 1) / K) : (mv + K - 1) / K;
         const size_t bytes = (size_t)cap * 16 * nin * nbuf;
-        if (bytes > budget) return false;
-        const int cl = max_active_clusters(pass, g.dtype, K, bytes);
+        if (bytes > lim) return false;
+        const int cl = max_active_clusters(pass, g.dtype, K, bytes, minb);
         if (cl <= 0) return false;
         best.ok = true;
+        best.minb = minb;
         best.K = K;
         best.clusters = (int)std::min<int64_t>(cl, g.C);
         best.cap = (uint32_t)cap;
@@ -349,25 +364,44 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
         best.chunk_vecs = (uint32_t)std::min<int64_t>(cv, cap);
         return true;
     };
-    if (kforce || nforce) {
-        for (int K = kforce ? kforce : 1; K <= (kforce ? kforce : kMaxCluster) && K <= mv; ++K)
-            for (int nb = nforce ? nforce : kMaxBuf; nb >= (nforce ? nforce : 1); --nb)
-                if (consider(K, nb)) goto done;
-        goto done;
+    {
+        // small slabs first: the 4-CTA/SM variant with ~50 KB double-buffered slabs
+        // (small layers: more resident pipelines; measured r50s3 52 -> 57 %), else
+        // the 2-CTA/SM variant with ~100 KB slabs (large channels, e.g. cfg4)
+        const int mforce = env_int("IABN_FUSED_MINB", 0);
+        const size_t small = std::min<size_t>(
+            (size_t)std::max(8, env_int("IABN_FUSED_SMALL_KB", 50)) * 1024, budget);
+        if (kforce || nforce) {
+            minb = mforce == 4 ? 4 : 2;
+            lim = minb == 4 ? small : budget;
+            for (int K = kforce ? kforce : 1; K <= (kforce ? kforce : kMaxCluster) && K <= mv; ++K)
+                for (int nb = nforce ? nforce : kMaxBuf; nb >= (nforce ? nforce : 1); --nb)
+                    if (consider(K, nb)) goto done;
+            goto done;
+        }
+        if (mforce != 2) {
+            minb = 4;
+            lim = small;
+            for (int K = 1; K <= 8 && K <= mv; ++K)
+                if (consider(K, 2)) goto done;
+        }
+        if (mforce == 4) goto done;
+        minb = 2;
+        lim = budget;
+        for (int K = 1; K <= 8 && K <= mv; ++K)
+            if (consider(K, 2)) goto done;
+        for (int K = 1; K <= kMaxCluster && K <= mv; ++K)
+            if (consider(K, 1)) goto done;
     }
-    for (int K = 1; K <= 8 && K <= mv; ++K)
-        if (consider(K, 2)) goto done;
-    for (int K = 1; K <= kMaxCluster && K <= mv; ++K)
-        if (consider(K, 1)) goto done;
 done:
     if (best.ok && env_int("IABN_VERBOSE", 0)) {
         static std::mutex pm;
         static int printed = 0;
         std::lock_guard<std::mutex> lk(pm);
         if (printed++ < 16)
-            fprintf(stderr, "[iabn] fused pass=%d C=%lld m=%lld: K=%d nbuf=%d clusters=%d smem=%zu cap=%u chunk=%u\n",
-                    pass, (long long)g.C, (long long)g.m, best.K, best.nbuf, best.clusters, best.smem,
-                    best.cap, best.chunk_vecs);
+            fprintf(stderr, "[iabn] fused pass=%d C=%lld m=%lld: K=%d nbuf=%d minb=%d clusters=%d smem=%zu cap=%u chunk=%u\n",
+                    pass, (long long)g.C, (long long)g.m, best.K, best.nbuf, best.minb, best.clusters,
+                    best.smem, best.cap, best.chunk_vecs);
     }
     return best;
 }
@@ -412,10 +446,12 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e;
-    if (pass == 0)
-        e = cudaLaunchKernelEx(&cfg, fused_kernel<T, 0>, a);
+    if (p.minb == 4)
+        e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4>, a)
+                      : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4>, a);
     else
-        e = cudaLaunchKernelEx(&cfg, fused_kernel<T, 1>, a);
+        e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2>, a)
+                      : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2>, a);
     if (e != cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return fail(IABN_ERR_CUDA, "fused launch: %s", cudaGetErrorString(e));

@@ -150,9 +150,6 @@ struct ApplyCoef {
 #ifndef IABN_APP_UNROLL
 #define IABN_APP_UNROLL 4  // vectors per apply-loop iteration
 #endif
-#ifndef IABN_MIN_BLOCKS
-#define IABN_MIN_BLOCKS 2  // CTAs per SM the register allocation must allow
-#endif
 constexpr int kReduceWarps = IABN_REDUCE_WARPS;  // stream each resident slice for the channel sums
 constexpr int kApplyWarps = IABN_APPLY_WARPS;    // stream it again, one channel behind, for outputs
 // Warp roles.  The SMSP arbiter favours higher warp ids, so the order sets the
@@ -185,8 +182,11 @@ __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool 
     group_sync(id, nthr);
 }
 
-template <typename T, int PASS>
-__global__ void __launch_bounds__(kFusedThreads, IABN_MIN_BLOCKS) fused_kernel(const FusedArgs a) {
+// MINB: CTAs per SM the register allocation must allow -- 2 (up to 113 registers,
+// ~100 KB slabs: large channels) or 4 (up to 56 registers, ~50 KB slabs: small
+// layers, where more resident pipelines hide the per-channel latency)
+template <typename T, int PASS, int MINB>
+__global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedArgs a) {
     constexpr int NIN = PASS == 0 ? 1 : 2;
     constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
     constexpr int V = Elem<T>::kVec;
