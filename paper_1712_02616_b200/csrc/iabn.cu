@@ -238,8 +238,22 @@ iabn_status check_ws(const Geom& g, void* ws, size_t ws_bytes, const WsLayout& w
 }
 
 // ====================================================================== fused planning
+// Experiment overrides (IABN_*), read once per process: no getenv on the hot path.
 int env_int(const char* name, int dflt) {
+    struct Entry {
+        const char* name;
+        bool set;
+        int val;
+    };
+    static std::mutex mu;
+    static Entry cache[32];
+    static int n = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < n; ++i)
+        if (cache[i].name == name || strcmp(cache[i].name, name) == 0)
+            return cache[i].set ? cache[i].val : dflt;
     const char* s = getenv(name);
+    if (n < 32) cache[n++] = Entry{name, s != nullptr, s ? atoi(s) : 0};
     return s ? atoi(s) : dflt;
 }
 

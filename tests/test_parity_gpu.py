@@ -341,3 +341,20 @@ def test_coop_schedule_query():
     d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: no TMA, small layer
     assert L.query_schedule(d, 0)[0] == 0  # opt-in only (measured slower)
     assert L.query_schedule(d, 0, ONE)[0] == 2 and L.query_schedule(d, 1, ONE)[0] == 2
+
+
+# ------------------------------------------------------------------ streaming at any plane alignment
+MISALIGNED = [
+    Case(8, 40, 196, dtype="bf16", seed=26),   # 392-byte planes: covering vectors, straddles
+    Case(4, 24, 49, dtype="bf16", seed=27),    # 98-byte planes
+    Case(3, 5, 7, dtype="bf16", seed=28),      # plane shorter than a vector: generic apply
+    Case(5, 6, 9, dtype="f32", seed=29),       # 36-byte planes
+    Case(2, 33, 1001, dtype="bf16", seed=30),  # long odd planes
+    Case(4, 37, 30, dtype="bf16", layout="NHWC", seed=31),  # NHWC, rows not 16-byte multiples
+    Case(4, 40, 30, dtype="bf16", layout="NHWC", seed=32),  # NHWC aligned, C/V = 5 vectors
+]
+
+
+@pytest.mark.parametrize("case", MISALIGNED, ids=lambda c: f"{c.layout}_{c.dtype}_{c.N}x{c.C}x{c.HW}")
+def test_streaming_any_alignment(case):
+    _check(case, STREAM)
