@@ -89,7 +89,15 @@ iabn_status device_facts(DevFacts** out) {
                              (const void*)fused_kernel<float, 0, 4>,
                              (const void*)fused_kernel<__nv_bfloat16, 0, 4>,
                              (const void*)fused_kernel<float, 1, 4>,
-                             (const void*)fused_kernel<__nv_bfloat16, 1, 4>};
+                             (const void*)fused_kernel<__nv_bfloat16, 1, 4>,
+                             (const void*)fused_kernel<float, 0, 2, true>,
+                             (const void*)fused_kernel<__nv_bfloat16, 0, 2, true>,
+                             (const void*)fused_kernel<float, 1, 2, true>,
+                             (const void*)fused_kernel<__nv_bfloat16, 1, 2, true>,
+                             (const void*)fused_kernel<float, 0, 4, true>,
+                             (const void*)fused_kernel<__nv_bfloat16, 0, 4, true>,
+                             (const void*)fused_kernel<float, 1, 4, true>,
+                             (const void*)fused_kernel<__nv_bfloat16, 1, 4, true>};
         for (const void* fn : fns) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -273,30 +281,38 @@ struct FusedPlan {
     int nbuf = 0;
     size_t smem = 0;
     int minb = 2;        // kernel variant: CTAs per SM its registers allow (2 or 4)
+    bool mis = false;    // planes not 16-byte aligned: covering-range kernels
+    uint32_t mis_w = 0;  // 16-byte slots per plane (MIS)
 };
 
-const void* fused_fn(int pass, int dtype, int minb) {
+template <bool MIS>
+const void* fused_fn_t(int pass, int dtype, int minb) {
     if (minb == 4) {
         if (pass == 0)
-            return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0, 4>
-                                     : (const void*)fused_kernel<__nv_bfloat16, 0, 4>;
-        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1, 4>
-                                 : (const void*)fused_kernel<__nv_bfloat16, 1, 4>;
+            return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0, 4, MIS>
+                                     : (const void*)fused_kernel<__nv_bfloat16, 0, 4, MIS>;
+        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1, 4, MIS>
+                                 : (const void*)fused_kernel<__nv_bfloat16, 1, 4, MIS>;
     }
     if (pass == 0)
-        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0, 2>
-                                 : (const void*)fused_kernel<__nv_bfloat16, 0, 2>;
-    return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1, 2>
-                             : (const void*)fused_kernel<__nv_bfloat16, 1, 2>;
+        return dtype == IABN_F32 ? (const void*)fused_kernel<float, 0, 2, MIS>
+                                 : (const void*)fused_kernel<__nv_bfloat16, 0, 2, MIS>;
+    return dtype == IABN_F32 ? (const void*)fused_kernel<float, 1, 2, MIS>
+                             : (const void*)fused_kernel<__nv_bfloat16, 1, 2, MIS>;
+}
+const void* fused_fn(int pass, int dtype, int minb, bool mis) {
+    return mis ? fused_fn_t<true>(pass, dtype, minb) : fused_fn_t<false>(pass, dtype, minb);
 }
 
 // Co-resident clusters of K CTAs with `smem` bytes of dynamic shared memory (cached).
-int max_active_clusters(int pass, int dtype, int K, size_t smem, int minb) {
+int max_active_clusters(int pass, int dtype, int K, size_t smem, int minb, bool mis) {
     static std::mutex mu;
     struct Key {
         int dev, pass, dtype, K;
         size_t smem;
-        int minb, val;
+        int minb;
+        bool mis;
+        int val;
     };
     static Key cache[512];
     static int ncache = 0;
@@ -305,7 +321,8 @@ int max_active_clusters(int pass, int dtype, int K, size_t smem, int minb) {
     std::lock_guard<std::mutex> lk(mu);
     for (int i = 0; i < ncache; ++i)
         if (cache[i].dev == dev && cache[i].pass == pass && cache[i].dtype == dtype &&
-            cache[i].K == K && cache[i].smem == smem && cache[i].minb == minb)
+            cache[i].K == K && cache[i].smem == smem && cache[i].minb == minb &&
+            cache[i].mis == mis)
             return cache[i].val;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)K, 1, 1);
@@ -319,11 +336,11 @@ int max_active_clusters(int pass, int dtype, int K, size_t smem, int minb) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, fused_fn(pass, dtype, minb), &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, fused_fn(pass, dtype, minb, mis), &cfg) != cudaSuccess) {
         cudaGetLastError();
         n = 0;
     }
-    if (ncache < 512) cache[ncache++] = Key{dev, pass, dtype, K, smem, minb, n};
+    if (ncache < 512) cache[ncache++] = Key{dev, pass, dtype, K, smem, minb, mis, n};
     return n;
 }
 
@@ -334,26 +351,38 @@ int max_active_clusters(int pass, int dtype, int K, size_t smem, int minb) {
 // of <= 8 CTAs pack the GPCs far better than 16.  So: the smallest K whose slice
 // double-buffers in the per-CTA budget; else (large channels) the smallest K
 // whose slice fits once.
-FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
+FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags) {
     FusedPlan best;
-    if (g.layout != IABN_NCHW || (g.HW * g.b) % 16 != 0) return best;
+    if (g.layout != IABN_NCHW) return best;
+    // planes not 16-byte aligned: each plane is held as the W aligned 16-byte slots that
+    // cover it (bulk copies need 16-byte alignment); needs whole planes per CTA and a
+    // tensor whose byte size is a multiple of 16 (the last plane's covering range)
+    // Measured slower than the streaming kernels for the small misaligned layers of
+    // cfg3/cfg5 (bf16 14x14, 7x7: profiles/r01_sweep_*), so taken only on request
+    // (IABN_FORCE_FUSED, or env IABN_FUSED_MIS=1).
+    const bool mis = (g.HW * g.b) % 16 != 0;
+    if (mis && ((g.E * g.b) % 16 != 0 ||
+                !((flags & IABN_FORCE_FUSED) || env_int("IABN_FUSED_MIS", 0) == 1)))
+        return best;
+    const int64_t W = (g.HW * g.b + 15) / 16 + 1;
     const int nin = pass == 0 ? 1 : 2;
-    const int64_t mv = g.m * g.b / 16;
+    const int64_t mv = mis ? g.N * W : g.m * g.b / 16;
     const size_t cap_bytes = (size_t)f.max_smem_optin - 4096;
     const size_t budget = std::min<size_t>(fused_budget_bytes(), cap_bytes);
     const int kforce = env_int("IABN_FUSED_K", 0);
     const int nforce = env_int("IABN_FUSED_NBUF", 0);
-    const int64_t pv = g.HW * g.b / 16;  // vectors per plane
+    const int64_t pv = mis ? W : g.HW * g.b / 16;  // vectors (slots) per plane
     const int64_t np = g.N;
     int minb = 2;
     size_t lim = budget;
     auto consider = [&](int K, int nbuf) -> bool {
         // slice: whole planes when N >= K (see cta_slice)
         const bool by_plane = np >= K;
+        if (mis && !by_plane) return false;
         const int64_t cap = by_plane ? pv * ((np + K - 1) / K) : (mv + K - 1) / K;
         const size_t bytes = (size_t)cap * 16 * nin * nbuf;
         if (bytes > lim) return false;
-        const int cl = max_active_clusters(pass, g.dtype, K, bytes, minb);
+        const int cl = max_active_clusters(pass, g.dtype, K, bytes, minb, mis);
         if (cl <= 0) return false;
         best.ok = true;
         best.minb = minb;
@@ -375,7 +404,10 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f) {
             cv = 2048 / nin;
         }
         cv = std::max<int64_t>(cv, (cap + kMaxChunks - 1) / kMaxChunks);
+        if (mis) cv = (cv + pv - 1) / pv * pv;  // whole planes
         best.chunk_vecs = (uint32_t)std::min<int64_t>(cv, cap);
+        best.mis = mis;
+        best.mis_w = (uint32_t)W;
         return true;
     };
     {
@@ -460,12 +492,23 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cudaError_t e;
-    if (p.minb == 4)
+    a.mis_w = p.mis_w;
+    a.hwb = (uint32_t)(a.HW * (int64_t)sizeof(T));
+    a.fd_w = fd32(p.mis ? p.mis_w : 1);
+    if (p.mis) {
+        if (p.minb == 4)
+            e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4, true>, a)
+                          : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4, true>, a);
+        else
+            e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2, true>, a)
+                          : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2, true>, a);
+    } else if (p.minb == 4) {
         e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4>, a)
                       : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4>, a);
-    else
+    } else {
         e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2>, a)
                       : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2>, a);
+    }
     if (e != cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return fail(IABN_ERR_CUDA, "fused launch: %s", cudaGetErrorString(e));
@@ -850,7 +893,7 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
     }
     FusedPlan p;
-    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 0, *c.dev);
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 0, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shape");
     if (p.ok) {
@@ -923,7 +966,7 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                           const float* gamma, const float* beta, const float* sv, float* dg,
                           float* db, float eps, float slope, uint32_t flags) {
     FusedPlan p;
-    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 1, *c.dev);
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 1, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shape");
     if (p.ok) {
@@ -1038,7 +1081,7 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     IABN_TRY(device_facts(&dev));
     FusedPlan p;
     if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_ONE_LAUNCH)))
-        p = fused_plan(g, pass, *dev);
+        p = fused_plan(g, pass, *dev, flags);
     *schedule = p.ok ? 1 : 0;
     *cluster = p.ok ? p.K : 0;
     if (!p.ok && !(flags & IABN_EVAL) && g.E < (1ll << 31) && coop_wanted(g, pass, flags, false))

@@ -59,6 +59,10 @@ struct FusedArgs {
     uint32_t nbuf;        // slab buffers in the ring (1..kMaxBuf)
     float momentum, eps, slope, inv_slope;
     uint32_t flags;
+    // planes not 16-byte aligned (MIS kernels): each plane of the slice occupies W = mis_w
+    // 16-byte slots holding the aligned range that covers it; hwb = HW * sizeof(T)
+    uint32_t mis_w, hwb;
+    FastDiv fd_w;
     uint32_t debug;  // experiments only (IABN_FUSED_DEBUG): 4 = record phase timestamps
                      // into `trace`
     unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
@@ -182,10 +186,42 @@ __device__ __forceinline__ void group_wait(uint64_t* bar, uint32_t parity, bool 
     group_sync(id, nthr);
 }
 
+// A plane of the MIS kernels: byte offset (in the tensor) of the aligned 16-byte range
+// covering plane pgi = n*C + c, and the head bytes before the plane's first element.
+struct MisPlane {
+    uint64_t a0;
+    uint32_t h;
+};
+__device__ __forceinline__ MisPlane mis_plane(uint64_t pgi, uint32_t hwb) {
+    const uint64_t B = pgi * hwb;
+    return {B & ~(uint64_t)15, (uint32_t)(B & 15)};
+}
+// element k of 16-byte slot i lies in the plane's bytes [h, h + hwb)
+template <typename T>
+__device__ __forceinline__ bool mis_valid(uint32_t i, int k, uint32_t h, uint32_t hwb) {
+    const uint32_t byte = i * 16u + (uint32_t)k * (uint32_t)sizeof(T);
+    return byte >= h && byte < h + hwb;
+}
+
+// one element of T from shared memory (byte address)
+template <typename T>
+__device__ __forceinline__ float lds_elem(uint32_t addr) {
+    if constexpr (sizeof(T) == 4) {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+        return v;
+    } else {
+        unsigned short h;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(addr));
+        return __uint_as_float((uint32_t)h << 16);
+    }
+}
+
 // MINB: CTAs per SM the register allocation must allow -- 2 (up to 113 registers,
 // ~100 KB slabs: large channels) or 4 (up to 56 registers, ~50 KB slabs: small
 // layers, where more resident pipelines hide the per-channel latency)
-template <typename T, int PASS, int MINB>
+// MIS: planes not 16-byte aligned (e.g. bf16 14x14): covering ranges, masked edges
+template <typename T, int PASS, int MINB, bool MIS = false>
 __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedArgs a) {
     constexpr int NIN = PASS == 0 ? 1 : 2;
     constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
@@ -208,7 +244,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     const uint32_t C = (uint32_t)a.C;
     const uint32_t nT = q < C ? (C - q + Q - 1) / Q : 0;  // channels of this cluster
     uint32_t vlo, vhi;
-    cta_slice(a.m / V, (uint32_t)a.HW / V, r, K, vlo, vhi);
+    if constexpr (MIS)  // whole planes of W slots each (the host ensures N >= K)
+        cta_slice(a.m / (uint32_t)a.HW * a.mis_w, a.mis_w, r, K, vlo, vhi);
+    else
+        cta_slice(a.m / V, (uint32_t)a.HW / V, r, K, vlo, vhi);
     const uint32_t nv = vhi - vlo;
     const int nch = (int)((nv + a.chunk_vecs - 1) / a.chunk_vecs);
     const size_t bufv = (size_t)NIN * a.cap;  // vectors per slab buffer
@@ -259,6 +298,26 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     const uint32_t c_hi = min(vhi, c_lo + a.chunk_vecs);
                     if (k == 0) IABN_TRACE(a, t, 0);
                     if (k == nch - 1) IABN_TRACE(a, t, 1);
+                    if constexpr (MIS) {
+                        // planes [n_lo, n_hi) of the chunk: copy each one's covering range
+                        const uint32_t n_lo = c_lo / a.mis_w, n_hi = c_hi / a.mis_w;
+                        uint32_t bytes = 0;
+                        for (uint32_t n = n_lo; n < n_hi; ++n) {
+                            const MisPlane mp = mis_plane((uint64_t)n * a.C + c, a.hwb);
+                            bytes += (uint32_t)(((mp.a0 + mp.h + a.hwb + 15) & ~(uint64_t)15) - mp.a0);
+                        }
+                        mbar_arrive_expect_tx(&full[b][k], bytes * NIN);
+                        for (uint32_t n = n_lo; n < n_hi; ++n) {
+                            const MisPlane mp = mis_plane((uint64_t)n * a.C + c, a.hwb);
+                            const uint32_t nb =
+                                (uint32_t)(((mp.a0 + mp.h + a.hwb + 15) & ~(uint64_t)15) - mp.a0);
+#pragma unroll
+                            for (int i = 0; i < NIN; ++i)
+                                bulk_g2s(buf + (size_t)i * a.cap + (n * a.mis_w - vlo),
+                                         (const char*)src[i] + mp.a0, nb, &full[b][k]);
+                        }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[b][k], (c_hi - c_lo) * 16u * NIN);
                     uint32_t j = c_lo * V;  // channel-space element
                     const uint32_t jend = c_hi * V;
@@ -377,9 +436,14 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             float2 ig2 = make_float2(0.f, 0.f), nb2 = ig2;
             if (PASS == 0) {
                 group_wait(&full[b][0], par, gw == 0, gb, RT);
-                float2 p0[NP];
-                Pairs<T>::load(lds128(xs), p0);
-                K0 = p0[0].x;  // shift: a sample of this slice (cancellation-free variance)
+                if constexpr (MIS) {  // first element of the slice's first plane
+                    const MisPlane mp = mis_plane((uint64_t)(vlo / a.mis_w) * a.C + c, a.hwb);
+                    K0 = lds_elem<T>(xs + mp.h);
+                } else {
+                    float2 p0[NP];
+                    Pairs<T>::load(lds128(xs), p0);
+                    K0 = p0[0].x;  // shift: a sample of this slice (cancellation-free variance)
+                }
             } else {
                 const InvAffine ia = inv_affine(__ldg(a.gamma + c), __ldg(a.beta + c), a.eps, a.flags);
                 ig2 = make_float2(ia.inv_g, ia.inv_g);
@@ -433,8 +497,59 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     }
                 }
             };
+            // MIS: a covering slot with elements outside the plane -- those are skipped
+            // (selects, not products: the slot's other bytes may hold anything)
+            auto reduce_vec_masked = [&](const uint4 zu, const uint4 du, uint32_t i, uint32_t h,
+                                         auto v2tag) {
+                constexpr bool V2 = decltype(v2tag)::value;
+                float zz[V], dd[V];
+                unpack<T>(zu, zz);
+                unpack<T>(du, dd);
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    const bool ok = mis_valid<T>(i, k, h, a.hwb);
+                    float* a1 = (k & 1) ? &s1[k >> 1].y : &s1[k >> 1].x;
+                    float* a2 = (k & 1) ? &s2[k >> 1].y : &s2[k >> 1].x;
+                    if (PASS == 0) {
+                        const float d = ok ? zz[k] - K0 : 0.f;
+                        *a1 += d;
+                        *a2 = fmaf(d, d, *a2);
+                    } else if (V2 && sizeof(T) == 2) {
+                        float* an = (k & 1) ? &sn[k >> 1].y : &sn[k >> 1].x;
+                        *a1 += ok ? dd[k] : 0.f;
+                        *an += (ok && zz[k] < 0.f) ? dd[k] : 0.f;
+                        *a2 += ok ? dd[k] * zz[k] : 0.f;
+                    } else {
+                        const float dy = zz[k] >= 0.f ? dd[k] : dd[k] * a.slope;
+                        *a1 += ok ? dy : 0.f;
+                        const float t2 = V2 ? dd[k] * zz[k]
+                                            : fmaf(dd[k] * zz[k], ig2.x, dy * nb2.x);
+                        *a2 += ok ? t2 : 0.f;
+                    }
+                }
+            };
             // all chunks of the slice; the 4-vector body issues its 8 shared loads first
             auto sweep = [&](auto v2tag) {
+                if constexpr (MIS) {
+                    const uint32_t n0 = vlo / a.mis_w;
+                    for (int k = 0; k < nch; ++k) {
+                        if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
+                        if (tid == 0 && k == 0) IABN_TRACE(a, t, 2);
+                        if (tid == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
+                        const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+                        for (uint32_t v = c_lo + tid; v < c_hi; v += RT) {
+                            const uint32_t jn = fdiv(v, a.fd_w), i = v - jn * a.mis_w;
+                            const uint32_t h = mis_plane((uint64_t)(n0 + jn) * a.C + c, a.hwb).h;
+                            const uint4 zu = lds128(xs + v * 16u);
+                            const uint4 du = PASS == 1 ? lds128(ds + v * 16u) : zu;
+                            if (i * 16u >= h && i * 16u + 16u <= h + a.hwb)
+                                reduce_vec(zu, du, v2tag);
+                            else if (i * 16u < h + a.hwb)
+                                reduce_vec_masked(zu, du, i, h, v2tag);
+                        }
+                    }
+                    return;
+                }
                 for (int k = 0; k < nch; ++k) {
                     if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
                     if (tid == 0 && k == 0) IABN_TRACE(a, t, 2);
@@ -494,7 +609,8 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 }
                 double out[NR];
                 if (PASS == 0) {
-                    write_raw_moments(out, (double)nv * V, (double)K0, S1, S2);
+                    const double cnt = MIS ? (double)(nv / a.mis_w) * (double)a.HW : (double)nv * V;
+                    write_raw_moments(out, cnt, (double)K0, S1, S2);
                 } else {
                     out[0] = S1;
                     out[1] = S2;
@@ -564,6 +680,63 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             const uint4 xu = lds128(xs + v * 16u);
             apply_vals(xu, PASS == 1 ? lds128(ds + v * 16u) : xu, dst);
         };
+        if constexpr (MIS) {
+            // each plane: its covering slots i < iend; interior slots are whole 16-byte
+            // stores, the (at most two) edge slots store only the plane's own elements
+            // (the rest of those 16 bytes belong to neighbouring channels)
+            const uint32_t W = a.mis_w, w_mod = W % AT;
+            for (int k = 0; k < nch; ++k) {
+                const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+                uint32_t off = 0;
+                for (uint32_t pb = c_lo; pb < c_hi; pb += W) {
+                    const MisPlane mp = mis_plane((uint64_t)((vlo + pb) / W) * a.C + cp, a.hwb);
+                    char* const gbase = (char*)a.out + mp.a0;
+                    const uint32_t iend = (mp.h + a.hwb + 15u) / 16u;
+                    for (uint32_t i = at >= off ? at - off : at + AT - off; i < iend; i += AT) {
+                        const uint4 xu = lds128(xs + (pb + i) * 16u);
+                        const uint4 du = PASS == 1 ? lds128(ds + (pb + i) * 16u) : xu;
+                        float2 w[NP];
+                        if (PASS == 0) {
+                            Pairs<T>::load_sub(xu, mu, w);
+#pragma unroll
+                            for (int j = 0; j < NP; ++j) {
+                                const float2 y = fma2(w[j], P, Q2);
+                                const float2 ay = mul2(y, sl2);
+                                w[j] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                            }
+                        } else {
+                            float2 dd[NP];
+                            Pairs<T>::load(xu, w);
+                            Pairs<T>::load(du, dd);
+                            const float2 cc2 = make_float2(mu, mu);
+#pragma unroll
+                            for (int j = 0; j < NP; ++j) {
+                                const bool px = w[j].x >= 0.f, py = w[j].y >= 0.f;
+                                const float2 al = make_float2(px ? P.x : Q2.x, py ? P.x : Q2.x);
+                                const float2 ka = make_float2(px ? P.y : Q2.y, py ? P.y : Q2.y);
+                                w[j] = fma2(al, dd[j], fma2(ka, w[j], cc2));
+                            }
+                        }
+                        T* const dst = (T*)(gbase + i * 16u);
+                        if (i * 16u >= mp.h && i * 16u + 16u <= mp.h + a.hwb) {
+                            st_vec(dst, Pairs<T>::store(w));
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < V; ++e)
+                                if (mis_valid<T>(i, e, mp.h, a.hwb))
+                                    st_scalar<T>(dst + e, (e & 1) ? w[e >> 1].y : w[e >> 1].x);
+                        }
+                    }
+                    off += w_mod;
+                    off = off >= AT ? off - AT : off;
+                }
+                __syncwarp();
+                if ((at & 31) == 0) mbar_arrive(&empty[b][k]);
+            }
+            if (at == 0) IABN_TRACE(a, s, 7);
+            if ((at & 31) == 0) mbar_arrive(&freed[slot]);
+            return;
+        }
         for (int k = 0; k < nch; ++k) {
             const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
             if (plane_loop) {

@@ -338,8 +338,8 @@ def test_coop_matches_streaming_bitwise(case):
 
 def test_coop_schedule_query():
     from paper_1712_02616_b200 import _lib as L
-    d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: no TMA, small layer
-    assert L.query_schedule(d, 0)[0] == 0  # opt-in only (measured slower)
+    d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: streaming by default
+    assert L.query_schedule(d, 0)[0] == 0  # one-launch / covering fused are opt-in (slower here)
     assert L.query_schedule(d, 0, ONE)[0] == 2 and L.query_schedule(d, 1, ONE)[0] == 2
 
 
@@ -358,3 +358,21 @@ MISALIGNED = [
 @pytest.mark.parametrize("case", MISALIGNED, ids=lambda c: f"{c.layout}_{c.dtype}_{c.N}x{c.C}x{c.HW}")
 def test_streaming_any_alignment(case):
     _check(case, STREAM)
+
+
+# ------------------------------------------------------------------ fused, planes not 16-byte aligned
+MIS_CASES = [
+    Case(8, 40, 196, dtype="bf16", seed=33),    # 392-byte planes (head 0 or 8 bytes)
+    Case(6, 24, 49, dtype="bf16", seed=34),     # 98-byte planes (7 x 7)
+    Case(4, 16, 9, dtype="f32", seed=35),       # 36-byte planes
+    Case(16, 8, 1001, dtype="bf16", seed=36),   # long odd planes, K > 1 planes per CTA
+    Case(32, 64, 49, dtype="f32", seed=37),     # 196-byte planes, many planes per slice
+]
+
+
+@pytest.mark.parametrize("case", MIS_CASES, ids=lambda c: f"{c.dtype}_{c.N}x{c.C}x{c.HW}")
+def test_fused_misaligned_planes(case):
+    from paper_1712_02616_b200 import _lib as L
+    d = L.desc(case.N, case.C, case.HW, L.BF16 if case.dtype == "bf16" else L.F32, L.NCHW)
+    assert L.query_schedule(d, 0, FUSED)[0] == 1 and L.query_schedule(d, 1, FUSED)[0] == 1
+    _check(case, FUSED)
