@@ -797,42 +797,60 @@ __device__ __forceinline__ void bwd_reduce_nhwc_body(const T* __restrict__ z, co
     }
     if (active) {
         int iter = 0;
-        for (int64_t r0 = rlo + ty; r0 < rhi; r0 += 16 * kUnroll) {
-            float fz[kUnroll][V], fd[kUnroll][V];
+        auto acc = [&](const float (&fz)[V], const float (&fd)[V]) {
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                const int64_t r = r0 + 16 * u;
-                if (r < rhi) {
-                    const int64_t off = r * C + c0;
-                    if constexpr (VEC) {
-                        unpack<T>(ld_vec(z + off), fz[u]);
-                        unpack<T>(ld_vec(dz + off), fd[u]);
-                    } else {
-                        fz[u][0] = ld_scalar<T>(z + off);
-                        fd[u][0] = ld_scalar<T>(dz + off);
-                    }
-                } else {
+            for (int k = 0; k < V; ++k) {
+                float dy, xh;
+                grad_terms(fz[k], fd[k], slope, inv_slope, ia[k], dy, xh);
+                a1[k] += dy;
+                a2[k] = fmaf(dy, xh, a2[k]);
+            }
+        };
+        auto flush = [&]() {
 #pragma unroll
-                    for (int k = 0; k < V; ++k) fz[u][k] = fd[u][k] = 0.f;
+            for (int k = 0; k < V; ++k) {
+                d1[k] += a1[k];
+                d2[k] += a2[k];
+                a1[k] = a2[k] = 0.f;
+            }
+        };
+        int64_t r0 = rlo + ty;
+        if constexpr (VEC) {
+            // raw loads of z and dz for kUnroll rows first (all in range), then the math
+            for (; r0 + 16 * (kUnroll - 1) < rhi; r0 += 16 * kUnroll) {
+                uint4 rz[kUnroll], rd[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    rz[u] = ld_vec_ro(z + (r0 + 16 * u) * C + c0);
+                    rd[u] = ld_vec_ro(dz + (r0 + 16 * u) * C + c0);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    float fz[V], fd[V];
+                    unpack<T>(rz[u], fz);
+                    unpack<T>(rd[u], fd);
+                    acc(fz, fd);
+                }
+                if (++iter == 4) {
+                    iter = 0;
+                    flush();
                 }
             }
-#pragma unroll
-            for (int u = 0; u < kUnroll; ++u)
-#pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    float dy, xh;
-                    grad_terms(fz[u][k], fd[u][k], slope, inv_slope, ia[k], dy, xh);
-                    a1[k] += dy;
-                    a2[k] = fmaf(dy, xh, a2[k]);
-                }
+        }
+        for (; r0 < rhi; r0 += 16) {
+            float fz[V], fd[V];
+            const int64_t off = r0 * C + c0;
+            if constexpr (VEC) {
+                unpack<T>(ld_vec_ro(z + off), fz);
+                unpack<T>(ld_vec_ro(dz + off), fd);
+            } else {
+                fz[0] = ld_scalar<T>(z + off);
+                fd[0] = ld_scalar<T>(dz + off);
+            }
+            acc(fz, fd);
             if (++iter == 16) {
                 iter = 0;
-#pragma unroll
-                for (int k = 0; k < V; ++k) {
-                    d1[k] += a1[k];
-                    d2[k] += a2[k];
-                    a1[k] = a2[k] = 0.f;
-                }
+                flush();
             }
         }
     }

@@ -376,3 +376,41 @@ def test_fused_misaligned_planes(case):
     d = L.desc(case.N, case.C, case.HW, L.BF16 if case.dtype == "bf16" else L.F32, L.NCHW)
     assert L.query_schedule(d, 0, FUSED)[0] == 1 and L.query_schedule(d, 1, FUSED)[0] == 1
     _check(case, FUSED)
+
+
+# ------------------------------------------------------------------ CUDA graphs
+@pytest.mark.parametrize("case", [Case(8, 32, 784, dtype="bf16", seed=40),
+                                  Case(4, 40, 196, dtype="bf16", seed=41),
+                                  Case(3, 24, 49, dtype="f32", layout="NHWC", seed=42)],
+                         ids=["fused", "streaming_misaligned", "nhwc"])
+def test_cuda_graph_capture(case):
+    """The calls only enqueue device work (no host synchronisation): a forward + backward
+    captured in a CUDA graph and replayed gives the eager results bit for bit."""
+    import paper_1712_02616_b200 as P
+    x, dz, p = inputs(case)
+    eager = run_gpu(case, x, dz, p)
+    xs, dzs = x.cuda(), dz.cuda()
+    g, b = p.gamma.cuda(), p.beta.cuda()
+    rm, rv = p.running_mean.cuda(), p.running_var.cuda()
+    kw = dict(eps=case.eps, slope=case.slope, gamma_mode=case.gamma_mode, layout=case.layout)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm-up: workspaces, kernel attributes, plans
+        z, _, sv = P.forward(xs.clone(), g, b, rm.clone(), rv.clone(), momentum=case.momentum, **kw)
+        P.backward(z, dzs.clone(), g, b, sv, **kw)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        z, sm, sv = P.forward(xs, g, b, rm, rv, momentum=case.momentum, **kw)
+        dx, dg, db = P.backward(z, dzs, g, b, sv, save_mean=sm, **kw)
+    xs.copy_(x.cuda())
+    dzs.copy_(dz.cuda())
+    rm.copy_(p.running_mean.cuda())
+    rv.copy_(p.running_var.cuda())
+    graph.replay()
+    torch.cuda.synchronize()
+    got = dict(z=z.cpu(), mean=sm.cpu(), var=sv.cpu(), rm=rm.cpu(), rv=rv.cpu(), dx=dx.cpu(),
+               dgamma=dg.cpu(), dbeta=db.cpu())
+    for k in got:
+        assert torch.equal(got[k], eager[k]), k
