@@ -548,27 +548,27 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                                 reduce_vec_masked(zu, du, i, h, v2tag);
                         }
                     }
-                    return;
-                }
-                for (int k = 0; k < nch; ++k) {
-                    if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
-                    if (tid == 0 && k == 0) IABN_TRACE(a, t, 2);
-                    if (tid == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
-                    const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-                    uint32_t v = c_lo + tid;
-                    for (; v + (kRU - 1) * RT < c_hi; v += kRU * RT) {
-                        uint4 zu[kRU], du[kRU];
-#pragma unroll
-                        for (int j = 0; j < kRU; ++j) {
-                            zu[j] = lds128(xs + (v + j * RT) * 16u);
-                            du[j] = PASS == 1 ? lds128(ds + (v + j * RT) * 16u) : zu[j];
+                } else {
+                    for (int k = 0; k < nch; ++k) {
+                        if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
+                        if (tid == 0 && k == 0) IABN_TRACE(a, t, 2);
+                        if (tid == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
+                        const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+                        uint32_t v = c_lo + tid;
+                        for (; v + (kRU - 1) * RT < c_hi; v += kRU * RT) {
+                            uint4 zu[kRU], du[kRU];
+    #pragma unroll
+                            for (int j = 0; j < kRU; ++j) {
+                                zu[j] = lds128(xs + (v + j * RT) * 16u);
+                                du[j] = PASS == 1 ? lds128(ds + (v + j * RT) * 16u) : zu[j];
+                            }
+    #pragma unroll
+                            for (int j = 0; j < kRU; ++j) reduce_vec(zu[j], du[j], v2tag);
                         }
-#pragma unroll
-                        for (int j = 0; j < kRU; ++j) reduce_vec(zu[j], du[j], v2tag);
-                    }
-                    for (; v < c_hi; v += RT) {
-                        const uint4 zu = lds128(xs + v * 16u);
-                        reduce_vec(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, v2tag);
+                        for (; v < c_hi; v += RT) {
+                            const uint4 zu = lds128(xs + v * 16u);
+                            reduce_vec(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, v2tag);
+                        }
                     }
                 }
             };
@@ -733,64 +733,62 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 __syncwarp();
                 if ((at & 31) == 0) mbar_arrive(&empty[b][k]);
             }
-            if (at == 0) IABN_TRACE(a, s, 7);
-            if ((at & 31) == 0) mbar_arrive(&freed[slot]);
-            return;
-        }
-        for (int k = 0; k < nch; ++k) {
-            const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-            if (plane_loop) {
-                // the chunk is whole planes: plane n of the channel is vectors [pb, pb + pv).
-                // Thread `at` takes the chunk's vectors u = at, at + AT, ... (u = pb - c_lo + v),
-                // i.e. in each plane the v with v = at - off (mod AT), off = (pb - c_lo) % AT
-                uint32_t n = (vlo + c_lo) / pv, off = 0;
-                const uint32_t pv_mod = pv % AT;
-                for (uint32_t pb = c_lo; pb < c_hi; pb += pv, ++n) {
-                    T* const dp = outc + (int64_t)n * chw;
-                    uint32_t v = at >= off ? at - off : at + AT - off;
-                    for (; v + (kAU - 1) * AT < pv; v += kAU * AT) {  // shared loads first
-                        uint4 xu[kAU], du[kAU];
-#pragma unroll
-                        for (int j = 0; j < kAU; ++j) {
-                            xu[j] = lds128(xs + (pb + v + j * AT) * 16u);
-                            du[j] = PASS == 1 ? lds128(ds + (pb + v + j * AT) * 16u) : xu[j];
+        } else {
+            for (int k = 0; k < nch; ++k) {
+                const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
+                if (plane_loop) {
+                    // the chunk is whole planes: plane n of the channel is vectors [pb, pb + pv).
+                    // Thread `at` takes the chunk's vectors u = at, at + AT, ... (u = pb - c_lo + v),
+                    // i.e. in each plane the v with v = at - off (mod AT), off = (pb - c_lo) % AT
+                    uint32_t n = (vlo + c_lo) / pv, off = 0;
+                    const uint32_t pv_mod = pv % AT;
+                    for (uint32_t pb = c_lo; pb < c_hi; pb += pv, ++n) {
+                        T* const dp = outc + (int64_t)n * chw;
+                        uint32_t v = at >= off ? at - off : at + AT - off;
+                        for (; v + (kAU - 1) * AT < pv; v += kAU * AT) {  // shared loads first
+                            uint4 xu[kAU], du[kAU];
+    #pragma unroll
+                            for (int j = 0; j < kAU; ++j) {
+                                xu[j] = lds128(xs + (pb + v + j * AT) * 16u);
+                                du[j] = PASS == 1 ? lds128(ds + (pb + v + j * AT) * 16u) : xu[j];
+                            }
+    #pragma unroll
+                            for (int j = 0; j < kAU; ++j) apply_vals(xu[j], du[j], dp + (v + j * AT) * V);
                         }
-#pragma unroll
-                        for (int j = 0; j < kAU; ++j) apply_vals(xu[j], du[j], dp + (v + j * AT) * V);
-                    }
-                    for (; v < pv; v += AT) apply_vec(pb + v, dp + v * V);
-                    off += pv_mod;
-                    off = off >= AT ? off - AT : off;
-                }
-            } else {
-                // output cursor: the thread visits v = c_lo + at, + AT, ... i.e. channel-space
-                // steps of AT*V elements: one plane wrap at most when the step <= HW, else
-                // the plane by division
-                const uint32_t step = AT * V;
-                const int64_t jump = (int64_t)step + chw - hw;  // step across a plane boundary
-                uint32_t v = c_lo + at;
-                const uint32_t j0 = (vlo + v) * V;
-                const uint32_t n0 = fdiv(j0, a.fd_hw);
-                uint32_t jsp = j0 - n0 * hw;
-                T* dst = outc + (int64_t)n0 * chw + jsp;
-                if (hw >= step) {
-                    for (; v < c_hi; v += AT) {
-                        apply_vec(v, dst);
-                        jsp += step;
-                        const bool wrap = jsp >= hw;
-                        jsp = wrap ? jsp - hw : jsp;
-                        dst += wrap ? jump : (int64_t)step;
+                        for (; v < pv; v += AT) apply_vec(pb + v, dp + v * V);
+                        off += pv_mod;
+                        off = off >= AT ? off - AT : off;
                     }
                 } else {
-                    for (; v < c_hi; v += AT) {
-                        const uint32_t j = (vlo + v) * V;
-                        const uint32_t n = fdiv(j, a.fd_hw);
-                        apply_vec(v, outc + (int64_t)n * chw + (j - n * hw));
+                    // output cursor: the thread visits v = c_lo + at, + AT, ... i.e. channel-space
+                    // steps of AT*V elements: one plane wrap at most when the step <= HW, else
+                    // the plane by division
+                    const uint32_t step = AT * V;
+                    const int64_t jump = (int64_t)step + chw - hw;  // step across a plane boundary
+                    uint32_t v = c_lo + at;
+                    const uint32_t j0 = (vlo + v) * V;
+                    const uint32_t n0 = fdiv(j0, a.fd_hw);
+                    uint32_t jsp = j0 - n0 * hw;
+                    T* dst = outc + (int64_t)n0 * chw + jsp;
+                    if (hw >= step) {
+                        for (; v < c_hi; v += AT) {
+                            apply_vec(v, dst);
+                            jsp += step;
+                            const bool wrap = jsp >= hw;
+                            jsp = wrap ? jsp - hw : jsp;
+                            dst += wrap ? jump : (int64_t)step;
+                        }
+                    } else {
+                        for (; v < c_hi; v += AT) {
+                            const uint32_t j = (vlo + v) * V;
+                            const uint32_t n = fdiv(j, a.fd_hw);
+                            apply_vec(v, outc + (int64_t)n * chw + (j - n * hw));
+                        }
                     }
                 }
+                __syncwarp();
+                if ((at & 31) == 0) mbar_arrive(&empty[b][k]);  // chunk k of buffer b may be refilled
             }
-            __syncwarp();
-            if ((at & 31) == 0) mbar_arrive(&empty[b][k]);  // chunk k of buffer b may be refilled
         }
         if (at == 0) IABN_TRACE(a, s, 7);
         if ((at & 31) == 0) mbar_arrive(&freed[slot]);  // coefficient slot may be rewritten
