@@ -56,14 +56,17 @@ def _desc(x: torch.Tensor, layout: str) -> L.Desc:
 _WS: dict[tuple, torch.Tensor] = {}
 
 
-def workspace(d: L.Desc, device: torch.device) -> tuple[int, int]:
+def workspace(d: L.Desc, device: torch.device, stream=None) -> tuple[int, int]:
+    """Scratch space of the call: one buffer per (device, stream), grown on demand.
+    Calls on one stream are ordered, so they may share it; calls on different
+    streams get different buffers (the library's calls are stream-ordered only)."""
     nbytes = max(L.workspace_bytes(d), 16)
-    key = (device.index, nbytes)
+    key = (device.index, _stream(stream))
     ws = _WS.get(key)
-    if ws is None:
+    if ws is None or ws.numel() < nbytes:
         ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
         _WS[key] = ws
-    return ws.data_ptr(), nbytes
+    return ws.data_ptr(), ws.numel()
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -154,7 +157,7 @@ def forward(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
         save_var = torch.empty(C, dtype=torch.float32, device=x.device)
     else:
         save_mean = save_var = None
-    ws, nb = workspace(d, x.device)
+    ws, nb = workspace(d, x.device, stream)
     args = [ctypes.byref(d), x.data_ptr(), z.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
             _ptr(running_mean), _ptr(running_var), _ptr(save_mean), _ptr(save_var), momentum, eps,
             slope, fl, ws, nb, _stream(stream)]
@@ -182,7 +185,7 @@ def backward(z: torch.Tensor, dz: torch.Tensor, gamma: torch.Tensor, beta: torch
     dgamma = torch.empty(C, dtype=torch.float32, device=z.device)
     dbeta = torch.empty(C, dtype=torch.float32, device=z.device)
     fl = _flags(gamma_mode, False, flags) | (L.SYNC_GLOBAL_PARAM_GRADS if global_param_grads else 0)
-    ws, nb = workspace(d, z.device)
+    ws, nb = workspace(d, z.device, stream)
     args = [ctypes.byref(d), z.data_ptr(), dz.data_ptr(), dx.data_ptr(), gamma.data_ptr(),
             beta.data_ptr(), _ptr(save_mean), save_var.data_ptr(), dgamma.data_ptr(),
             dbeta.data_ptr(), eps, slope, fl, ws, nb, _stream(stream)]
@@ -198,7 +201,7 @@ def forward_reduce(x: torch.Tensor, *, layout: str = "NCHW", stream=None) -> tor
     """Local raw moments, fp64 [C, 3] = (count, sum, sum of squares)."""
     d = _desc(x, layout)
     stats = torch.empty(d.c, 3, dtype=torch.float64, device=x.device)
-    ws, nb = workspace(d, x.device)
+    ws, nb = workspace(d, x.device, stream)
     L.call("iabn_forward_reduce", ctypes.byref(d), x.data_ptr(), stats.data_ptr(), ws, nb,
            _stream(stream))
     return stats
@@ -213,7 +216,7 @@ def forward_apply(x: torch.Tensor, stats_global: torch.Tensor, gamma, beta, runn
     z = x if out is None else out
     save_mean = torch.empty(C, dtype=torch.float32, device=x.device)
     save_var = torch.empty(C, dtype=torch.float32, device=x.device)
-    ws, nb = workspace(d, x.device)
+    ws, nb = workspace(d, x.device, stream)
     assert stats_global.dtype == torch.float64 and stats_global.numel() == 3 * C
     L.call("iabn_forward_apply", ctypes.byref(d), x.data_ptr(), z.data_ptr(),
            stats_global.data_ptr(), _f32(gamma, C, "gamma").data_ptr(),
@@ -230,7 +233,7 @@ def backward_reduce(z, dz, gamma, beta, *, eps=1e-5, slope=0.01, gamma_mode="abs
     d = _desc(z, layout)
     C = d.c
     sums = torch.empty(2 * C + 1, dtype=torch.float64, device=z.device)
-    ws, nb = workspace(d, z.device)
+    ws, nb = workspace(d, z.device, stream)
     L.call("iabn_backward_reduce", ctypes.byref(d), z.data_ptr(), dz.data_ptr(),
            _f32(gamma, C, "gamma").data_ptr(), _f32(beta, C, "beta").data_ptr(), sums.data_ptr(),
            eps, slope, _flags(gamma_mode, False, flags), ws, nb, _stream(stream))
@@ -245,7 +248,7 @@ def backward_apply(z, dz, sums_global, sums_local, gamma, beta, save_var, *, eps
     dx = dz if dx is None else dx
     dgamma = torch.empty(C, dtype=torch.float32, device=z.device)
     dbeta = torch.empty(C, dtype=torch.float32, device=z.device)
-    ws, nb = workspace(d, z.device)
+    ws, nb = workspace(d, z.device, stream)
     fl = _flags(gamma_mode, False, flags) | (L.SYNC_GLOBAL_PARAM_GRADS if global_param_grads else 0)
     L.call("iabn_backward_apply", ctypes.byref(d), z.data_ptr(), dz.data_ptr(), dx.data_ptr(),
            sums_global.data_ptr(), _ptr(sums_local), _f32(gamma, C, "gamma").data_ptr(),

@@ -414,3 +414,27 @@ def test_cuda_graph_capture(case):
                dgamma=dg.cpu(), dbeta=db.cpu())
     for k in got:
         assert torch.equal(got[k], eager[k]), k
+
+
+def test_two_streams_concurrently():
+    """Calls on different streams use different workspaces: two layers run
+    concurrently give the results each gives alone."""
+    import paper_1712_02616_b200 as P
+    cases = [Case(4, 24, 196, dtype="bf16", seed=43), Case(4, 24, 196, dtype="bf16", seed=44)]
+    alone = [run_gpu(c, *inputs(c)) for c in cases]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    torch.cuda.synchronize()
+    for c, s in zip(cases, streams):
+        x, dz, p = inputs(c)
+        with torch.cuda.stream(s):
+            xd, dzd = x.cuda(), dz.cuda()
+            g, b = p.gamma.cuda(), p.beta.cuda()
+            rm, rv = p.running_mean.cuda(), p.running_var.cuda()
+            z, sm, sv = P.forward(xd, g, b, rm, rv, momentum=c.momentum, eps=c.eps, slope=c.slope)
+            dx, dg, db = P.backward(z, dzd, g, b, sv, eps=c.eps, slope=c.slope)
+            outs.append(dict(z=z, dx=dx, dgamma=dg, dbeta=db, mean=sm, var=sv))
+    torch.cuda.synchronize()
+    for o, a in zip(outs, alone):
+        for k in o:
+            assert torch.equal(o[k].cpu(), a[k]), k
