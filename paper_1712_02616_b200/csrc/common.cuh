@@ -176,6 +176,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialisation may start while the previous kernel of the stream finishes; every
+// kernel calls this before its first global-memory access (read or write), which
+// waits until the previous grid has completed and its writes are visible.  A no-op
+// for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 16-byte shared-memory load by 32-bit shared address (volatile: stays after the
 // mbarrier wait that makes the data visible)
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {

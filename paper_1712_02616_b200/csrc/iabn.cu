@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <utility>
 #include <string>
 
 #include "iabn.h"
@@ -265,6 +266,29 @@ int env_int(const char* name, int dflt) {
     return s ? atoi(s) : dflt;
 }
 
+// Kernel launch with programmatic stream serialisation (PDL): the kernel may be
+// scheduled while the previous kernel on the stream drains; it waits in pdl_wait()
+// before touching global memory.  IABN_PDL=0 launches plainly (experiments).
+bool pdl_enabled() {
+    static const bool on = env_int("IABN_PDL", 1) != 0;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: check_launch
+}
+
 // Shared-memory budget per CTA for the slab ring: ~100 KB keeps two CTAs per SM.
 size_t fused_budget_bytes() {
     static const size_t budget = (size_t)std::max(8, env_int("IABN_FUSED_SMEM_KB", 100)) * 1024;
@@ -484,13 +508,15 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     cfg.blockDim = dim3(kFusedThreads, 1, 1);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = p.K;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e;
     a.mis_w = p.mis_w;
     a.hwb = (uint32_t)(a.HW * (int64_t)sizeof(T));
@@ -589,19 +615,19 @@ iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cuda
         const dim3 grid((unsigned)g.C, (unsigned)S);
         const FastDiv fd = fd32(g.HW);
         if (vec)
-            stats_nchw_kernel<T, true><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.HW,
+            launch_pdl(stats_nchw_kernel<T, true>, grid, kThreads, 0, st, (const T*)x, g.C, g.HW,
                                                                   (uint32_t)g.m, fd, part);
         else  // planes not 16-byte aligned: masked covering vectors
-            nchw_cover_kernel<T, 0><<<grid, kThreads, 0, st>>>(
+            launch_pdl(nchw_cover_kernel<T, 0>, grid, kThreads, 0, st,
                 (const T*)x, nullptr, nullptr, nullptr, g.C, g.HW, g.N, g.E, 0.f, 1.f, 1.f, 0u,
                 cover_fd(g), part);
     } else {
         const int V = vec ? 16 / g.b : 1;
         const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
         if (vec)
-            stats_nhwc_kernel<T, true><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.m, part);
+            launch_pdl(stats_nhwc_kernel<T, true>, grid, kThreads, 0, st, (const T*)x, g.C, g.m, part);
         else
-            stats_nhwc_kernel<T, false><<<grid, kThreads, 0, st>>>((const T*)x, g.C, g.m, part);
+            launch_pdl(stats_nhwc_kernel<T, false>, grid, kThreads, 0, st, (const T*)x, g.C, g.m, part);
     }
     return check_launch("stats kernel");
 }
@@ -616,22 +642,22 @@ iabn_status launch_bwd_reduce(const Geom& g, int S, const void* z, const void* d
         const dim3 grid((unsigned)g.C, (unsigned)S);
         const FastDiv fd = fd32(g.HW);
         if (vec)
-            bwd_reduce_nchw_kernel<T, true><<<grid, kThreads, 0, st>>>(
+            launch_pdl(bwd_reduce_nchw_kernel<T, true>, grid, kThreads, 0, st,
                 (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, (uint32_t)g.m, fd, eps, slope,
                 inv_slope, flags, part);
         else  // planes not 16-byte aligned: masked covering vectors
-            nchw_cover_kernel<T, 1><<<grid, kThreads, 0, st>>>(
+            launch_pdl(nchw_cover_kernel<T, 1>, grid, kThreads, 0, st,
                 (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, g.N, g.E, eps, slope,
                 inv_slope, flags, cover_fd(g), part);
     } else {
         const int V = vec ? 16 / g.b : 1;
         const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
         if (vec)
-            bwd_reduce_nhwc_kernel<T, true><<<grid, kThreads, 0, st>>>(
+            launch_pdl(bwd_reduce_nhwc_kernel<T, true>, grid, kThreads, 0, st,
                 (const T*)z, (const T*)dz, gamma, beta, g.C, g.m, eps, slope, inv_slope, flags,
                 part);
         else
-            bwd_reduce_nhwc_kernel<T, false><<<grid, kThreads, 0, st>>>(
+            launch_pdl(bwd_reduce_nhwc_kernel<T, false>, grid, kThreads, 0, st,
                 (const T*)z, (const T*)dz, gamma, beta, g.C, g.m, eps, slope, inv_slope, flags,
                 part);
     }
@@ -681,21 +707,21 @@ iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4
         T* zp = (T*)z + off;
         const int grid = apply_grid(E, g.b, sms);
         if (g.layout == IABN_NCHW && g.HW >= 16 / g.b) {  // any alignment (straddles handled)
-            fwd_apply_rows_kernel<T><<<grid, kThreads, 0, st>>>(
+            launch_pdl(fwd_apply_rows_kernel<T>, grid, kThreads, 0, st,
                 xp, zp, coef, E, (uint32_t)g.HW, (uint32_t)g.C, fh, fc, slope);
         } else if (g.layout == IABN_NCHW) {
             if (al)
-                fwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 0, true>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
             else
-                fwd_apply_kernel<T, 0, false><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 0, false>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
         } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
-            fwd_apply_nhwc_kernel<T><<<nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st>>>(
+            launch_pdl(fwd_apply_nhwc_kernel<T>, nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st,
                 xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope);
         } else {
             if (al)
-                fwd_apply_kernel<T, 1, true><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 1, true>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
             else
-                fwd_apply_kernel<T, 1, false><<<grid, kThreads, 0, st>>>(xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 1, false>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
         }
         IABN_TRY(check_launch("fwd_apply kernel"));
     }
@@ -719,22 +745,22 @@ iabn_status launch_bwd_apply(const Geom& g, const void* z, const void* dz, void*
         T* dxp = (T*)dx + off;
         const int grid = apply_grid(E, g.b, sms);
         if (g.layout == IABN_NCHW && g.HW >= 16 / g.b) {  // any alignment (straddles handled)
-            bwd_apply_rows_kernel<T><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, (uint32_t)g.HW,
+            launch_pdl(bwd_apply_rows_kernel<T>, grid, kThreads, 0, st, zp, dzp, dxp, coef, E, (uint32_t)g.HW,
                                                                (uint32_t)g.C, fh, fc, slope, inv_slope);
         } else if (g.layout == IABN_NCHW) {
             if (al)
-                bwd_apply_kernel<T, 0, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+                launch_pdl(bwd_apply_kernel<T, 0, true>, grid, kThreads, 0, st, zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
             else
-                bwd_apply_kernel<T, 0, false><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+                launch_pdl(bwd_apply_kernel<T, 0, false>, grid, kThreads, 0, st, zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
         } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
-            bwd_apply_nhwc_kernel<T><<<nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st>>>(
+            launch_pdl(bwd_apply_nhwc_kernel<T>, nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st,
                 zp, dzp, dxp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope,
                 inv_slope);
         } else {
             if (al)
-                bwd_apply_kernel<T, 1, true><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+                launch_pdl(bwd_apply_kernel<T, 1, true>, grid, kThreads, 0, st, zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
             else
-                bwd_apply_kernel<T, 1, false><<<grid, kThreads, 0, st>>>(zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
+                launch_pdl(bwd_apply_kernel<T, 1, false>, grid, kThreads, 0, st, zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
         }
         IABN_TRY(check_launch("bwd_apply kernel"));
     }
@@ -877,7 +903,7 @@ iabn_status fwd_from_partials(const Ctx& c, const double* part, int S, const voi
                               uint32_t flags) {
     FwdCoefArgs a{part, S, c.g.C, gamma, beta, rm, rv, sm, sv, wsp<float4>(c, c.w.coef),
                   momentum, eps, flags};
-    fwd_coef_kernel<<<wgrid(c.g.C), 128, 0, c.st>>>(a);
+    launch_pdl(fwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
     IABN_TRY(check_launch("fwd_coef kernel"));
     return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
 }
@@ -887,7 +913,7 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
                          const float* beta, float* rm, float* rv, float* sm, float* sv,
                          float momentum, float eps, float slope, uint32_t flags) {
     if (flags & IABN_EVAL) {
-        eval_coef_kernel<<<cgrid(c.g.C), 128, 0, c.st>>>(c.g.C, gamma, beta, rm, rv, eps, flags,
+        launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv, eps, flags,
                                                          wsp<float4>(c, c.w.coef));
         IABN_TRY(check_launch("eval_coef kernel"));
         return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
@@ -956,7 +982,7 @@ iabn_status bwd_from_sums(const Ctx& c, const double* glob, int Sg, const double
                           float* dg, float* db, float eps, float slope, uint32_t flags) {
     BwdCoefArgs a{glob, Sg, loc, Sl, count_ptr, count, c.g.C, gamma, beta, sv, dg, db,
                   wsp<float4>(c, c.w.coef), eps, flags};
-    bwd_coef_kernel<<<wgrid(c.g.C), 128, 0, c.st>>>(a);
+    launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
     IABN_TRY(check_launch("bwd_coef kernel"));
     return launch_bwd_apply<T>(c.g, z, dz, dx, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
 }
@@ -1138,7 +1164,7 @@ iabn_status iabn_fold_conv(int64_t cout, int64_t k_per_out, const float* w, cons
     }
     DevFacts* dev = nullptr;
     IABN_TRY(device_facts(&dev));
-    fold_conv_kernel<<<(unsigned)cout, kThreads, 0, (cudaStream_t)stream>>>(
+    launch_pdl(fold_conv_kernel, (unsigned)cout, kThreads, 0, (cudaStream_t)stream,
         w, bias, running_mean, running_var, gamma, beta, eps, flags, k_per_out, w_out, bias_out);
     return check_launch("fold_conv kernel");
 }
@@ -1152,7 +1178,7 @@ iabn_status iabn_forward_reduce(const iabn_desc* desc, const void* x, double* st
     if (!stats) return fail(IABN_ERR_INVALID_ARG, "stats is NULL");
     IABN_TRY(attach_device(c));
     IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
-    combine_kernel<3><<<wgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
+    launch_pdl(combine_kernel<3>, wgrid(c.g.C), 128, 0, c.st, wsp<double>(c, c.w.part), c.S, c.g.C, stats,
                                                       -1.0);
     return check_launch("combine kernel");
 }
@@ -1187,7 +1213,7 @@ iabn_status iabn_backward_reduce(const iabn_desc* desc, const void* z, const voi
     double* part = wsp<double>(c, c.w.part);
     IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
                       flags, part, c.st));
-    combine_kernel<2><<<wgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, sums, (double)c.g.m);
+    launch_pdl(combine_kernel<2>, wgrid(c.g.C), 128, 0, c.st, part, c.S, c.g.C, sums, (double)c.g.m);
     return check_launch("combine kernel");
 }
 
@@ -1264,7 +1290,7 @@ iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, con
     IABN_TRY(attach_device(c));
     double* stats = wsp<double>(c, c.w.stats);
     IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
-    combine_kernel<3><<<wgrid(c.g.C), 128, 0, c.st>>>(wsp<double>(c, c.w.part), c.S, c.g.C, stats,
+    launch_pdl(combine_kernel<3>, wgrid(c.g.C), 128, 0, c.st, wsp<double>(c, c.w.part), c.S, c.g.C, stats,
                                                       -1.0);
     IABN_TRY(check_launch("combine kernel"));
     IABN_TRY(allreduce_f64(stats, (size_t)c.g.C * 3, comm, c.st));
@@ -1290,7 +1316,7 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
     double* glob = wsp<double>(c, c.w.sums_glob);
     IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
                       flags, part, c.st));
-    combine_kernel<2><<<wgrid(c.g.C), 128, 0, c.st>>>(part, c.S, c.g.C, loc, (double)c.g.m);
+    launch_pdl(combine_kernel<2>, wgrid(c.g.C), 128, 0, c.st, part, c.S, c.g.C, loc, (double)c.g.m);
     IABN_TRY(check_launch("combine kernel"));
     const size_t nb = (size_t)(2 * c.g.C + 1) * sizeof(double);
     const cudaError_t e = cudaMemcpyAsync(glob, loc, nb, cudaMemcpyDeviceToDevice, c.st);

@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     // every CTA's barriers are initialised before any peer may arrive on them
     cluster_arrive_release();
     cluster_wait_acquire();
+    pdl_wait();  // the prologue above overlaps the previous kernel's tail
 
     if (warp == kProducerWarp) {
         // ================================================ producer: slab t into buffer t % nbuf,

@@ -223,6 +223,7 @@ template <typename T, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     stats_nchw_kernel(const T* __restrict__ x, int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw,
                       double* __restrict__ part) {
+    pdl_wait();
     stats_nchw_body<T, VEC>(x, C, HW, m, fd_hw, part, hw_blk());
 }
 
@@ -323,6 +324,7 @@ __device__ __forceinline__ void stats_nhwc_body(const T* __restrict__ x, int64_t
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(kThreads)
     stats_nhwc_kernel(const T* __restrict__ x, int64_t C, int64_t rows, double* __restrict__ part) {
+    pdl_wait();
     stats_nhwc_body<T, VEC>(x, C, rows, part, hw_blk());
 }
 
@@ -355,6 +357,7 @@ __device__ __forceinline__ int64_t warp_channel() {
 template <int NV>
 __global__ void combine_kernel(const double* __restrict__ part, int S, int64_t C,
                                double* __restrict__ out, double extra) {
+    pdl_wait();
     const int64_t c = warp_channel();
     if (c == 0 && threadIdx.x == 0 && extra >= 0.0) out[NV * C] = extra;
     if (c >= C) return;
@@ -431,6 +434,7 @@ __device__ __forceinline__ void fwd_coef_body(const FwdCoefArgs& a, int64_t c) {
     update_running(a.running_mean, a.running_var, c, mean, var, cnt, a.momentum, a.flags);
 }
 __global__ void fwd_coef_kernel(FwdCoefArgs a) {
+    pdl_wait();
     const int64_t c = warp_channel();
     if (c < a.C) fwd_coef_body(a, c);
 }
@@ -440,6 +444,7 @@ __global__ void eval_coef_kernel(int64_t C, const float* __restrict__ gamma,
                                  const float* __restrict__ beta, const float* __restrict__ rm,
                                  const float* __restrict__ rv, float eps, uint32_t flags,
                                  float4* __restrict__ coef) {
+    pdl_wait();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= C) return;
     const double A = gamma_eff(gamma[c], eps, flags) / sqrt((double)rv[c] + (double)eps);
@@ -518,6 +523,7 @@ template <typename T, int LAYOUT, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
                      FastDiv fd_c, float slope) {
+    pdl_wait();
     fwd_apply_body<T, LAYOUT, ALIGNED>(x, z, coef, E, fd_hw, fd_c, slope, hw_blk());
 }
 
@@ -615,6 +621,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E,
                           uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope) {
+    pdl_wait();
     fwd_apply_rows_body<T>(x, z, coef, E, HW, C, fd_hw, fd_c, slope, hw_blk());
 }
 
@@ -765,6 +772,7 @@ __global__ void __launch_bounds__(kThreads)
                            int64_t C, int64_t HW, uint32_t m, FastDiv fd_hw, float eps,
                            float slope, float inv_slope, uint32_t flags,
                            double* __restrict__ part) {
+    pdl_wait();
     bwd_reduce_nchw_body<T, VEC>(z, dz, gamma, beta, C, HW, m, fd_hw, eps, slope, inv_slope, flags, part, hw_blk());
 }
 
@@ -881,6 +889,7 @@ __global__ void __launch_bounds__(kThreads)
                            const float* __restrict__ gamma, const float* __restrict__ beta,
                            int64_t C, int64_t rows, float eps, float slope, float inv_slope,
                            uint32_t flags, double* __restrict__ part) {
+    pdl_wait();
     bwd_reduce_nhwc_body<T, VEC>(z, dz, gamma, beta, C, rows, eps, slope, inv_slope, flags, part, hw_blk());
 }
 
@@ -937,6 +946,7 @@ __device__ __forceinline__ void bwd_coef_body(const BwdCoefArgs& a, int64_t c) {
     a.dgamma[c] = (float)(gamma_sign(a.gamma[c], a.flags) * l2);
 }
 __global__ void bwd_coef_kernel(BwdCoefArgs a) {
+    pdl_wait();
     const int64_t c = warp_channel();
     if (c < a.C) bwd_coef_body(a, c);
 }
@@ -999,6 +1009,7 @@ template <typename T, int LAYOUT, bool ALIGNED>
 __global__ void __launch_bounds__(kThreads)
     bwd_apply_kernel(const T* __restrict__ z, const T* dz, T* dx, const float4* __restrict__ coef,
                      uint32_t E, FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope) {
+    pdl_wait();
     bwd_apply_body<T, LAYOUT, ALIGNED>(z, dz, dx, coef, E, fd_hw, fd_c, slope, inv_slope, hw_blk());
 }
 
@@ -1080,6 +1091,7 @@ __global__ void __launch_bounds__(kThreads)
     bwd_apply_rows_kernel(const T* __restrict__ z, const T* dz, T* dx,
                           const float4* __restrict__ coef, uint32_t E, uint32_t HW, uint32_t C,
                           FastDiv fd_hw, FastDiv fd_c, float slope, float inv_slope) {
+    pdl_wait();
     bwd_apply_rows_body<T>(z, dz, dx, coef, E, HW, C, fd_hw, fd_c, slope, inv_slope, hw_blk());
 }
 
@@ -1196,6 +1208,7 @@ __global__ void __launch_bounds__(kThreads)
                       const float* __restrict__ gamma, const float* __restrict__ beta, int64_t C,
                       int64_t HW, int64_t N, int64_t E, float eps, float slope, float inv_slope,
                       uint32_t flags, FastDiv fdw, double* __restrict__ part) {
+    pdl_wait();
     nchw_cover_body<T, PASS>(in0, in1, gamma, beta, C, HW, N, E, eps, slope, inv_slope, flags,
                              fdw, part, hw_blk());
 }
@@ -1209,6 +1222,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_nhwc_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
                           uint32_t cv, float slope) {
+    pdl_wait();
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = V / 2;
     const uint32_t stride = gridDim.x * kThreads;
@@ -1250,6 +1264,7 @@ __global__ void __launch_bounds__(kThreads)
     bwd_apply_nhwc_kernel(const T* __restrict__ z, const T* dz, T* dx,
                           const float4* __restrict__ coef, uint32_t nvec, uint32_t cv,
                           float slope, float inv_slope) {
+    pdl_wait();
     constexpr int V = Elem<T>::kVec;
     const uint32_t stride = gridDim.x * kThreads;
     uint32_t v = blockIdx.x * kThreads + threadIdx.x;
@@ -1298,6 +1313,7 @@ __global__ void __launch_bounds__(kThreads)
                      const float* __restrict__ rv, const float* __restrict__ gamma,
                      const float* __restrict__ beta, float eps, uint32_t flags, int64_t kper,
                      float* w_out, float* bias_out) {
+    pdl_wait();
     const int64_t k = blockIdx.x;
     const double sd = gamma_eff(gamma[k], eps, flags) / sqrt((double)rv[k] + (double)eps);
     const float s = (float)sd;
