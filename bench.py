@@ -86,7 +86,7 @@ def load_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-SCHEDULES = ["streaming", "fused", "one-launch"]  # iabn_query_schedule codes
+SCHEDULES = ["streaming", "fused", "one-launch", "grid-resident"]  # iabn_query_schedule codes
 
 
 def load_traffic(config: str):

@@ -28,6 +28,7 @@ VARIANT_I = 1 << 5
 FORCE_STREAMING = 1 << 8
 FORCE_FUSED = 1 << 9
 FORCE_ONE_LAUNCH = 1 << 10
+FORCE_RESIDENT = 1 << 11
 
 EXPORTS = ["iabn_version", "iabn_status_string", "iabn_last_error", "iabn_launch_count",
            "iabn_workspace_bytes", "iabn_query_schedule", "iabn_forward", "iabn_backward",

@@ -22,6 +22,7 @@
 
 #include "iabn.h"
 #include "kernels_coop.cuh"
+#include "kernels_gres.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_stream.cuh"
 
@@ -103,6 +104,16 @@ iabn_status device_facts(DevFacts** out) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         }
+        const void* gres[] = {(const void*)gres_kernel<float, 0>,
+                              (const void*)gres_kernel<__nv_bfloat16, 0>,
+                              (const void*)gres_kernel<float, 1>,
+                              (const void*)gres_kernel<__nv_bfloat16, 1>};
+        for (const void* fn : gres) {  // static shared memory of these is ~4.2 KB
+            cudaFuncAttributes fa = {};
+            cudaFuncGetAttributes(&fa, fn);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 f.max_smem_optin - (int)fa.sharedSizeBytes);
+        }
         e = cudaGetLastError();
         if (e != cudaSuccess)
             return fail(IABN_ERR_CUDA, "kernel attribute setup: %s", cudaGetErrorString(e));
@@ -178,11 +189,16 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 struct WsLayout {
     size_t part, stats, sums_loc, sums_glob, coef, bar, total;
 };
+// grid-resident NHWC schedule: at most this many CTAs (2 per SM of a 148-SM B200; a
+// device constant so that workspace sizes do not depend on the device)
+constexpr int64_t kGresMaxG = 296;
+
 WsLayout ws_layout(const Geom& g, int S) {
     WsLayout w;
     size_t off = 0;
     w.part = off;
-    off += align256((size_t)S * g.C * 3 * sizeof(double));
+    const int64_t rec = g.layout == IABN_NHWC ? std::max<int64_t>(S, kGresMaxG) : S;
+    off += align256((size_t)rec * g.C * 3 * sizeof(double));
     w.stats = off;
     off += align256((size_t)g.C * 3 * sizeof(double));
     w.sums_loc = off;
@@ -607,6 +623,79 @@ iabn_status launch_coop(const Geom& g, CoopArgs a, cudaStream_t st, int sms) {
 // covering vectors per plane of the misaligned NCHW reductions (nchw_cover_body)
 FastDiv cover_fd(const Geom& g) { return make_fastdiv((uint32_t)(g.HW / (16 / g.b) + 2)); }
 
+// ====================================================================== grid-resident NHWC
+// The whole NHWC tensor resident in the grid's shared memory (kernels_gres.cuh):
+// returns the grid (0 = not possible): rows split over G CTAs of at most
+// IABN_GRES_KB (default 96) KB of input each, 2 CTAs per SM, G <= kGresMaxG.
+int gres_grid(const Geom& g, int pass, uint32_t flags, const DevFacts& f) {
+    if (g.layout != IABN_NHWC || !vec_ok(g) || g.E >= (1ll << 31)) return 0;
+    if (flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_ONE_LAUNCH | IABN_EVAL))
+        return 0;
+    // opt-in: measured against the streaming kernels (tools/shape_graph.py, graph replay,
+    // DenseNet-like NHWC shapes at N = 32) it wins for bf16 layers of ~13 MB (1.1-1.4x)
+    // and loses for tiny and fp32 layers, and whole-network sweeps come out slower
+    if (!(flags & IABN_FORCE_RESIDENT) && env_int("IABN_GRES", 0) != 1) return 0;
+    const int64_t row_bytes = g.C * g.b * (pass == 0 ? 1 : 2);
+    if (g.C * g.b / 16 > kThreads) return 0;  // one 16-byte column per thread at least
+    const int64_t per = (int64_t)std::max(8, env_int("IABN_GRES_KB", 96)) * 1024;
+    const int64_t maxg = std::min<int64_t>(std::min<int64_t>(kGresMaxG, 2 * (int64_t)f.sms), g.m);
+    int64_t G = (g.m * row_bytes + per - 1) / per;
+    G = std::max<int64_t>(G, std::min<int64_t>(f.sms, g.m));  // at least one CTA per SM
+    if (G > maxg) return 0;
+    // the largest slice must fit (rows split as evenly as possible)
+    if ((g.m + G - 1) / G * row_bytes > per) return 0;
+    return (int)G;
+}
+
+// Persistent grid-barrier state, one slot per stream (allocated and zeroed once per
+// device; a stream keeps its slot, so launches on one stream are ordered).
+GridBar* gres_bar(cudaStream_t st) {
+    constexpr int kSlotsPerDev = 256;
+    static std::mutex mu;
+    static GridBar* base[kMaxDev] = {};
+    static cudaStream_t owner[kMaxDev][kSlotsPerDev];
+    static int used[kMaxDev] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!base[dev]) {
+        GridBar* p = nullptr;
+        if (cudaMalloc(&p, kSlotsPerDev * sizeof(GridBar)) != cudaSuccess) return nullptr;
+        if (cudaMemset(p, 0, kSlotsPerDev * sizeof(GridBar)) != cudaSuccess) return nullptr;
+        base[dev] = p;
+    }
+    for (int i = 0; i < used[dev]; ++i)
+        if (owner[dev][i] == st) return base[dev] + i;
+    if (used[dev] == kSlotsPerDev) return nullptr;
+    owner[dev][used[dev]] = st;
+    return base[dev] + used[dev]++;
+}
+
+template <typename T, int PASS>
+iabn_status launch_gres(const Geom& g, int G, GresArgs a, cudaStream_t st) {
+    a.bar = gres_bar(st);
+    if (!a.bar) return fail(IABN_ERR_CUDA, "grid-barrier state unavailable");
+    const int64_t row_bytes = g.C * g.b * (PASS == 0 ? 1 : 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)G, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)((g.m + G - 1) / G * row_bytes);
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gres_kernel<T, PASS>, a);
+    if (e != cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return fail(IABN_ERR_CUDA, "grid-resident kernel: %s", cudaGetErrorString(e));
+    }
+    return check_launch(PASS == 0 ? "gres_kernel<fwd>" : "gres_kernel<bwd>");
+}
+
 // ====================================================================== streaming launches
 template <typename T>
 iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cudaStream_t st) {
@@ -943,6 +1032,23 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         a.flags = flags;
         return launch_fused<T>(0, p, a, c.st);
     }
+    if (const int G = gres_grid(c.g, 0, flags, *c.dev)) {
+        GresArgs a{};
+        a.in0 = x;
+        a.out = z;
+        a.C = c.g.C;
+        a.rows = c.g.m;
+        a.cv = (uint32_t)(c.g.C * c.g.b / 16);
+        a.slope = slope;
+        a.inv_slope = 1.0f / slope;
+        a.eps = eps;
+        a.flags = flags;
+        a.part = wsp<double>(c, c.w.part);
+        a.coef = wsp<float4>(c, c.w.coef);
+        a.fwd = FwdCoefArgs{a.part, G, c.g.C, gamma, beta, rm, rv, sm, sv, a.coef, momentum, eps,
+                            flags};
+        return launch_gres<T, 0>(c.g, G, a, c.st);
+    }
     if (coop_wanted(c.g, 0, flags, false) && c.g.E < (1ll << 31)) {
         CoopArgs a{};
         a.in0 = x;
@@ -1016,6 +1122,26 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
         return launch_fused<T>(1, p, a, c.st);
     }
     double* part = wsp<double>(c, c.w.part);
+    if (const int G = gres_grid(c.g, 1, flags, *c.dev)) {
+        GresArgs a{};
+        a.in0 = z;
+        a.in1 = dz;
+        a.out = dx;
+        a.C = c.g.C;
+        a.rows = c.g.m;
+        a.cv = (uint32_t)(c.g.C * c.g.b / 16);
+        a.slope = slope;
+        a.inv_slope = 1.0f / slope;
+        a.eps = eps;
+        a.flags = flags;
+        a.gamma = gamma;
+        a.beta = beta;
+        a.part = part;
+        a.coef = wsp<float4>(c, c.w.coef);
+        a.bwd = BwdCoefArgs{part, G, part, G, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg,
+                            db, a.coef, eps, flags};
+        return launch_gres<T, 1>(c.g, G, a, c.st);
+    }
     if (coop_wanted(c.g, 1, flags, false) && c.g.E < (1ll << 31)) {
         CoopArgs a{};
         a.in0 = z;
@@ -1112,6 +1238,7 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     *cluster = p.ok ? p.K : 0;
     if (!p.ok && !(flags & IABN_EVAL) && g.E < (1ll << 31) && coop_wanted(g, pass, flags, false))
         *schedule = 2;
+    if (!p.ok && *schedule == 0 && gres_grid(g, pass, flags, *dev) > 0) *schedule = 3;
     return IABN_OK;
 }
 

@@ -438,3 +438,36 @@ def test_two_streams_concurrently():
     for o, a in zip(outs, alone):
         for k in o:
             assert torch.equal(o[k].cpu(), a[k]), k
+
+
+# ------------------------------------------------------------------ grid-resident NHWC schedule
+GRES_CASES = [
+    Case(8, 64, 49, dtype="bf16", layout="NHWC", seed=45),    # cv = 8
+    Case(8, 96, 49, dtype="bf16", layout="NHWC", seed=46),    # cv = 12: 252 active threads
+    Case(4, 40, 196, dtype="f32", layout="NHWC", seed=47),    # cv = 10
+    Case(32, 128, 196, dtype="bf16", layout="NHWC", seed=48), # DenseNet bottleneck, 14 x 14
+    Case(3, 1024, 5, dtype="f32", layout="NHWC", seed=49),    # few rows, wide rows (cv = 256)
+    Case(5, 24, 7, dtype="f32", layout="NHWC", stress="offset", seed=50),  # |mean|/std = 1e3
+]
+
+
+RESIDENT = 1 << 11
+
+
+@pytest.mark.parametrize("case", GRES_CASES, ids=lambda c: f"{c.dtype}_{c.N}x{c.C}x{c.HW}")
+def test_grid_resident_nhwc(case):
+    from paper_1712_02616_b200 import _lib as L
+    d = L.desc(case.N, case.C, case.HW, L.BF16 if case.dtype == "bf16" else L.F32, L.NHWC)
+    assert L.query_schedule(d, 0)[0] == 0  # opt-in
+    assert L.query_schedule(d, 0, RESIDENT)[0] == 3 and L.query_schedule(d, 1, RESIDENT)[0] == 3
+    _check(case, RESIDENT)
+
+
+def test_grid_resident_matches_streaming_bitwise_stats():
+    """Same per-channel statistics up to the combine order; outputs agree to fp32 rounding."""
+    case = Case(16, 64, 196, dtype="f32", layout="NHWC", seed=51)
+    x, dz, p = inputs(case)
+    a = run_gpu(case, x, dz, p, flags=RESIDENT)
+    b = run_gpu(case, x, dz, p, flags=STREAM)
+    for k in ("z", "dx"):
+        assert (a[k] - b[k]).abs().max().item() <= 1e-5 * b[k].abs().max().item(), k
