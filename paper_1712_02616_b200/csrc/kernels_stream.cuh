@@ -340,10 +340,21 @@ __device__ __forceinline__ void warp_split_sum(const double* __restrict__ part, 
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-#pragma unroll 4
-    for (int s = lane; s < S; s += 32)
+    // 8 records per lane in flight (loads first, then the adds in the same order)
+    for (int s0 = lane; s0 < S; s0 += 32 * 8) {
+        double v[8][NV];
 #pragma unroll
-        for (int k = 0; k < NV; ++k) acc[k] += part[((int64_t)s * C + c) * NV + k];
+        for (int u = 0; u < 8; ++u) {
+            const int s = s0 + 32 * u;
+#pragma unroll
+            for (int k = 0; k < NV; ++k)
+                v[u][k] = s < S ? __ldcg(part + ((int64_t)s * C + c) * NV + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int k = 0; k < NV; ++k) acc[k] += v[u][k];
+    }
 #pragma unroll
     for (int k = 0; k < NV; ++k)
 #pragma unroll
