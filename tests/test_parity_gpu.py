@@ -471,3 +471,29 @@ def test_grid_resident_matches_streaming_bitwise_stats():
     b = run_gpu(case, x, dz, p, flags=STREAM)
     for k in ("z", "dx"):
         assert (a[k] - b[k]).abs().max().item() <= 1e-5 * b[k].abs().max().item(), k
+
+
+# ------------------------------------------------------------------ sync variant through NCCL
+@pytest.mark.parametrize("case", [Case(4, 24, 196, dtype="f32", seed=52),
+                                  Case(4, 40, 64, dtype="bf16", layout="NHWC", seed=53)],
+                         ids=["nchw_f32", "nhwc_bf16"])
+def test_sync_through_nccl_single_rank(case):
+    """iabn_forward_sync / iabn_backward_sync with a real NCCL communicator of one rank
+    (the all-reduce runs; results equal the oracle on the batch)."""
+    import paper_1712_02616_b200 as P
+    comm = P.Comm.create(1, 0, P.Comm.unique_id())
+    try:
+        x, dz, p = inputs(case)
+        xd, dzd = x.cuda(), dz.cuda()
+        g, b = p.gamma.cuda(), p.beta.cuda()
+        rm, rv = p.running_mean.cuda(), p.running_var.cuda()
+        z, sm, sv = P.forward(xd, g, b, rm, rv, momentum=case.momentum, eps=case.eps,
+                              slope=case.slope, layout=case.layout, comm=comm)
+        dx, dg, db = P.backward(z, dzd, g, b, sv, eps=case.eps, slope=case.slope,
+                                layout=case.layout, comm=comm)
+        torch.cuda.synchronize()
+        got = dict(z=z.cpu(), mean=sm.cpu(), var=sv.cpu(), rm=rm.cpu(), rv=rv.cpu(),
+                   dx=dx.cpu(), dgamma=dg.cpu(), dbeta=db.cpu())
+        compare(case, got, run_oracle(case, x, dz, p), p)
+    finally:
+        comm.close()
