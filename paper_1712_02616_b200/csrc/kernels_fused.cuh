@@ -532,21 +532,58 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             // all chunks of the slice; the 4-vector body issues its 8 shared loads first
             auto sweep = [&](auto v2tag) {
                 if constexpr (MIS) {
-                    const uint32_t n0 = vlo / a.mis_w;
+                    // slot v of the slice = (plane jn, slot i) with v = jn W + i; a cursor
+                    // steps it by RT (no division in the loop); the plane's head offset
+                    // is h0 + jn dh (mod 16); kMRU slots' shared loads issued first
+                    constexpr int kMRU = MINB == 4 ? 2 : 4;
+                    const uint32_t W = a.mis_w, n0 = vlo / W;
+                    const uint32_t h0 = mis_plane((uint64_t)n0 * a.C + c, a.hwb).h;
+                    const uint32_t dh = (uint32_t)(((uint64_t)a.C * a.hwb) & 15u);
+                    const uint32_t qp = RT / W, qr = RT % W;
+                    auto one = [&](const uint4 zu, const uint4 du, uint32_t si, uint32_t sj) {
+                        const uint32_t h = (h0 + sj * dh) & 15u;
+                        if (si * 16u >= h && si * 16u + 16u <= h + a.hwb)
+                            reduce_vec(zu, du, v2tag);
+                        else if (si * 16u < h + a.hwb)
+                            reduce_vec_masked(zu, du, si, h, v2tag);
+                    };
                     for (int k = 0; k < nch; ++k) {
                         if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
                         if (tid == 0 && k == 0) IABN_TRACE(a, t, 2);
                         if (tid == 0 && k == nch - 1) IABN_TRACE(a, t, 3);
                         const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-                        for (uint32_t v = c_lo + tid; v < c_hi; v += RT) {
-                            const uint32_t jn = fdiv(v, a.fd_w), i = v - jn * a.mis_w;
-                            const uint32_t h = mis_plane((uint64_t)(n0 + jn) * a.C + c, a.hwb).h;
+                        uint32_t v = c_lo + tid;
+                        uint32_t jn = fdiv(v, a.fd_w), i = v - jn * W;
+                        for (; v + (kMRU - 1) * RT < c_hi;) {
+                            uint4 zu[kMRU], du[kMRU];
+                            uint32_t iu[kMRU], ju[kMRU];
+#pragma unroll
+                            for (int q = 0; q < kMRU; ++q) {
+                                zu[q] = lds128(xs + v * 16u);
+                                du[q] = PASS == 1 ? lds128(ds + v * 16u) : zu[q];
+                                iu[q] = i;
+                                ju[q] = jn;
+                                v += RT;
+                                i += qr;
+                                jn += qp;
+                                if (i >= W) {
+                                    i -= W;
+                                    ++jn;
+                                }
+                            }
+#pragma unroll
+                            for (int q = 0; q < kMRU; ++q) one(zu[q], du[q], iu[q], ju[q]);
+                        }
+                        for (; v < c_hi;) {
                             const uint4 zu = lds128(xs + v * 16u);
-                            const uint4 du = PASS == 1 ? lds128(ds + v * 16u) : zu;
-                            if (i * 16u >= h && i * 16u + 16u <= h + a.hwb)
-                                reduce_vec(zu, du, v2tag);
-                            else if (i * 16u < h + a.hwb)
-                                reduce_vec_masked(zu, du, i, h, v2tag);
+                            one(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, i, jn);
+                            v += RT;
+                            i += qr;
+                            jn += qp;
+                            if (i >= W) {
+                                i -= W;
+                                ++jn;
+                            }
                         }
                     }
                 } else {
@@ -682,54 +719,84 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             apply_vals(xu, PASS == 1 ? lds128(ds + v * 16u) : xu, dst);
         };
         if constexpr (MIS) {
-            // each plane: its covering slots i < iend; interior slots are whole 16-byte
-            // stores, the (at most two) edge slots store only the plane's own elements
-            // (the rest of those 16 bytes belong to neighbouring channels)
-            const uint32_t W = a.mis_w, w_mod = W % AT;
+            // slots of the slice by a stride cursor (as in the reduce); interior slots are
+            // whole 16-byte stores, the (at most two) edge slots of a plane store only its
+            // own elements (the rest of those 16 bytes belong to neighbouring channels)
+            constexpr int kMAU = MINB == 4 ? 2 : 4;
+            const uint32_t W = a.mis_w, n0 = vlo / W;
+            const uint64_t B0 = ((uint64_t)n0 * a.C + cp) * a.hwb;  // plane 0's first byte
+            const uint64_t dB = (uint64_t)a.C * a.hwb;               // bytes between planes
+            const uint32_t h0 = (uint32_t)(B0 & 15u), dh = (uint32_t)(dB & 15u);
+            const uint32_t qp = AT / W, qr = AT % W;
+            auto one = [&](const uint4 xu, const uint4 du, uint32_t si, uint32_t sj) {
+                const uint32_t h = (h0 + sj * dh) & 15u;
+                if (si * 16u >= h + a.hwb) return;  // slot beyond the plane's cover
+                float2 w[NP];
+                if (PASS == 0) {
+                    Pairs<T>::load_sub(xu, mu, w);
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        const float2 y = fma2(w[j], P, Q2);
+                        const float2 ay = mul2(y, sl2);
+                        w[j] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                    }
+                } else {
+                    float2 dd[NP];
+                    Pairs<T>::load(xu, w);
+                    Pairs<T>::load(du, dd);
+                    const float2 cc2 = make_float2(mu, mu);
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        const bool px = w[j].x >= 0.f, py = w[j].y >= 0.f;
+                        const float2 al = make_float2(px ? P.x : Q2.x, py ? P.x : Q2.x);
+                        const float2 ka = make_float2(px ? P.y : Q2.y, py ? P.y : Q2.y);
+                        w[j] = fma2(al, dd[j], fma2(ka, w[j], cc2));
+                    }
+                }
+                T* const dst = (T*)((char*)a.out + (B0 + sj * dB - h) + si * 16u);
+                if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) {
+                    st_vec(dst, Pairs<T>::store(w));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < V; ++e)
+                        if (mis_valid<T>(si, e, h, a.hwb))
+                            st_scalar<T>(dst + e, (e & 1) ? w[e >> 1].y : w[e >> 1].x);
+                }
+            };
             for (int k = 0; k < nch; ++k) {
                 const uint32_t c_lo = k * a.chunk_vecs, c_hi = min(nv, c_lo + a.chunk_vecs);
-                uint32_t off = 0;
-                for (uint32_t pb = c_lo; pb < c_hi; pb += W) {
-                    const MisPlane mp = mis_plane((uint64_t)((vlo + pb) / W) * a.C + cp, a.hwb);
-                    char* const gbase = (char*)a.out + mp.a0;
-                    const uint32_t iend = (mp.h + a.hwb + 15u) / 16u;
-                    for (uint32_t i = at >= off ? at - off : at + AT - off; i < iend; i += AT) {
-                        const uint4 xu = lds128(xs + (pb + i) * 16u);
-                        const uint4 du = PASS == 1 ? lds128(ds + (pb + i) * 16u) : xu;
-                        float2 w[NP];
-                        if (PASS == 0) {
-                            Pairs<T>::load_sub(xu, mu, w);
+                uint32_t v = c_lo + at;
+                uint32_t jn = fdiv(v, a.fd_w), i = v - jn * W;
+                for (; v + (kMAU - 1) * AT < c_hi;) {
+                    uint4 xu[kMAU], du[kMAU];
+                    uint32_t iu[kMAU], ju[kMAU];
 #pragma unroll
-                            for (int j = 0; j < NP; ++j) {
-                                const float2 y = fma2(w[j], P, Q2);
-                                const float2 ay = mul2(y, sl2);
-                                w[j] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
-                            }
-                        } else {
-                            float2 dd[NP];
-                            Pairs<T>::load(xu, w);
-                            Pairs<T>::load(du, dd);
-                            const float2 cc2 = make_float2(mu, mu);
-#pragma unroll
-                            for (int j = 0; j < NP; ++j) {
-                                const bool px = w[j].x >= 0.f, py = w[j].y >= 0.f;
-                                const float2 al = make_float2(px ? P.x : Q2.x, py ? P.x : Q2.x);
-                                const float2 ka = make_float2(px ? P.y : Q2.y, py ? P.y : Q2.y);
-                                w[j] = fma2(al, dd[j], fma2(ka, w[j], cc2));
-                            }
-                        }
-                        T* const dst = (T*)(gbase + i * 16u);
-                        if (i * 16u >= mp.h && i * 16u + 16u <= mp.h + a.hwb) {
-                            st_vec(dst, Pairs<T>::store(w));
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < V; ++e)
-                                if (mis_valid<T>(i, e, mp.h, a.hwb))
-                                    st_scalar<T>(dst + e, (e & 1) ? w[e >> 1].y : w[e >> 1].x);
+                    for (int q = 0; q < kMAU; ++q) {
+                        xu[q] = lds128(xs + v * 16u);
+                        du[q] = PASS == 1 ? lds128(ds + v * 16u) : xu[q];
+                        iu[q] = i;
+                        ju[q] = jn;
+                        v += AT;
+                        i += qr;
+                        jn += qp;
+                        if (i >= W) {
+                            i -= W;
+                            ++jn;
                         }
                     }
-                    off += w_mod;
-                    off = off >= AT ? off - AT : off;
+#pragma unroll
+                    for (int q = 0; q < kMAU; ++q) one(xu[q], du[q], iu[q], ju[q]);
+                }
+                for (; v < c_hi;) {
+                    const uint4 xu = lds128(xs + v * 16u);
+                    one(xu, PASS == 1 ? lds128(ds + v * 16u) : xu, i, jn);
+                    v += AT;
+                    i += qr;
+                    jn += qp;
+                    if (i >= W) {
+                        i -= W;
+                        ++jn;
+                    }
                 }
                 __syncwarp();
                 if ((at & 31) == 0) mbar_arrive(&empty[b][k]);

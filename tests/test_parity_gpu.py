@@ -367,6 +367,7 @@ MIS_CASES = [
     Case(4, 16, 9, dtype="f32", seed=35),       # 36-byte planes
     Case(16, 8, 1001, dtype="bf16", seed=36),   # long odd planes, K > 1 planes per CTA
     Case(32, 64, 49, dtype="f32", seed=37),     # 196-byte planes, many planes per slice
+    Case(4, 1500, 49, dtype="bf16", seed=38),   # more channels than clusters: slots reused
 ]
 
 
