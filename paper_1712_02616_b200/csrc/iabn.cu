@@ -397,12 +397,11 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags)
     // planes not 16-byte aligned: each plane is held as the W aligned 16-byte slots that
     // cover it (bulk copies need 16-byte alignment); needs whole planes per CTA and a
     // tensor whose byte size is a multiple of 16 (the last plane's covering range)
-    // Measured slower than the streaming kernels for the small misaligned layers of
-    // cfg3/cfg5 (bf16 14x14, 7x7: profiles/r01_sweep_*), so taken only on request
-    // (IABN_FORCE_FUSED, or env IABN_FUSED_MIS=1).
+    // (faster than the streaming kernels on the misaligned layers of cfg3/cfg5: bf16
+    // 14x14 and 7x7, fp32 7x7 -- whole-network sweeps 8-13 %; env IABN_FUSED_MIS=0 off)
     const bool mis = (g.HW * g.b) % 16 != 0;
     if (mis && ((g.E * g.b) % 16 != 0 ||
-                !((flags & IABN_FORCE_FUSED) || env_int("IABN_FUSED_MIS", 0) == 1)))
+                (!(flags & IABN_FORCE_FUSED) && env_int("IABN_FUSED_MIS", 1) == 0)))
         return best;
     const int64_t W = (g.HW * g.b + 15) / 16 + 1;
     const int nin = pass == 0 ? 1 : 2;

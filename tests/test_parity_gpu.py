@@ -338,8 +338,8 @@ def test_coop_matches_streaming_bitwise(case):
 
 def test_coop_schedule_query():
     from paper_1712_02616_b200 import _lib as L
-    d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: streaming by default
-    assert L.query_schedule(d, 0)[0] == 0  # one-launch / covering fused are opt-in (slower here)
+    d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: covering-range fused kernels
+    assert L.query_schedule(d, 0)[0] == 1  # the one-launch schedule is opt-in (slower)
     assert L.query_schedule(d, 0, ONE)[0] == 2 and L.query_schedule(d, 1, ONE)[0] == 2
 
 
