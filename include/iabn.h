@@ -105,9 +105,13 @@ enum {
                                          barriers, inputs re-read from L2); bitwise equal to
                                          streaming; IABN_ERR_UNSUPPORTED for 2^31 elements
                                          or more */
-    IABN_FORCE_RESIDENT = 1u << 11    /* NHWC: the whole tensor resident in the grid's shared
+    IABN_FORCE_RESIDENT = 1u << 11,   /* NHWC: the whole tensor resident in the grid's shared
                                          memory, one cooperative launch (falls back to
                                          streaming when it does not fit) */
+    /* iabn_{forward,backward}_sync: the channel-resident kernels with the cross-rank
+       exchange inside the kernel (see "fused-collective sync" below) instead of reduce
+       kernels + ncclAllReduce + apply kernels.  Also enabled by env IABN_SYNC_FUSED=1. */
+    IABN_SYNC_FUSED = 1u << 12
 };
 
 typedef struct iabn_desc {
@@ -182,6 +186,47 @@ IABN_API iabn_status iabn_backward_sync(const iabn_desc *desc, const void *z, co
                                const float *save_var, float *dgamma, float *dbeta, float eps,
                                float slope, uint32_t flags, void *ws, size_t ws_bytes,
                                void *stream, iabn_comm comm);
+
+/* ------------------------------------------------------------------ fused-collective sync
+ * With IABN_SYNC_FUSED (NCHW shapes the channel-resident schedule takes, at most 8
+ * ranks on one node) iabn_{forward,backward}_sync run ONE kernel per pass: each rank
+ * keeps its shard's channel slab in shared memory while the cluster owning channel c
+ * stores its record -- (count, sum x, sum x^2) forward, (sum dy, sum dy y) backward,
+ * fp64 -- into every rank's record buffer over NVLink (CUDA IPC mappings, exchanged
+ * with ncclAllGather at the first call and whenever C grows: collective), waits for the
+ * nranks records of c, folds them in rank order (bit-identical on every rank) and
+ * writes its outputs from the still-resident slab: 2*E*b forward and 3*E*b backward
+ * HBM bytes instead of 3*E*b / 5*E*b, no separate collective launch.  Requirements
+ * (the caller's, as for NCCL counts): every rank calls with the same desc (equal
+ * shards) and flags, in the same order.  A rank that never makes the call makes the
+ * others trap after ~20 s instead of hanging.  Shapes the fused schedule cannot take
+ * use the reduce / all-reduce / apply path.
+ *
+ * One-GPU emulation (tests and single-GPU measurement of the same kernels and record
+ * protocol): the nranks shards of one tensor -- x, z, dz, dx hold nranks * desc->n
+ * samples, shard r = samples [r n, (r+1) n) -- processed by one cooperative launch whose
+ * clusters are split among virtual ranks that exchange records through local memory.
+ * desc describes ONE shard.  Outputs: z / dx over the whole tensor; save_mean/save_var
+ * and the running statistics once ([C], global); dgamma/dbeta [nranks][C] (row r = shard
+ * r's contribution, or the global sums in every row with IABN_SYNC_GLOBAL_PARAM_GRADS).
+ * Exchange buffers are library-owned, per (device, stream); the first call of a
+ * (stream, nranks, larger C) allocates them synchronously (not inside a graph capture).
+ * Errors: as iabn_forward / iabn_backward (workspace sized for the whole tensor), plus
+ * IABN_ERR_INVALID_ARG (nranks outside [1, 8], IABN_EVAL) and IABN_ERR_UNSUPPORTED
+ * (NHWC, or a shard the channel-resident schedule cannot take). */
+IABN_API iabn_status iabn_forward_sync_emulated(const iabn_desc *desc, int nranks, const void *x,
+                                                void *z, const float *gamma, const float *beta,
+                                                float *running_mean, float *running_var,
+                                                float *save_mean, float *save_var, float momentum,
+                                                float eps, float slope, uint32_t flags, void *ws,
+                                                size_t ws_bytes, void *stream);
+IABN_API iabn_status iabn_backward_sync_emulated(const iabn_desc *desc, int nranks, const void *z,
+                                                 const void *dz, void *dx, const float *gamma,
+                                                 const float *beta, const float *save_mean,
+                                                 const float *save_var, float *dgamma,
+                                                 float *dbeta, float eps, float slope,
+                                                 uint32_t flags, void *ws, size_t ws_bytes,
+                                                 void *stream);
 
 /* ------------------------------------------------------------------ split phase
  * The sync path in pieces, for callers with their own collective (e.g. a

@@ -6,9 +6,11 @@ behind the C ABI of include/iabn.h.  This package is its thin Python binding.
 """
 from . import _lib
 from .functional import (Comm, InPlaceABN, InPlaceABNFunction, backward, backward_apply,
-                         backward_reduce, fold_conv, forward, forward_apply, forward_reduce,
-                         inplace_abn, layout_of)
+                         backward_reduce, backward_sync_emulated, fold_conv, forward,
+                         forward_apply, forward_reduce, forward_sync_emulated, inplace_abn,
+                         layout_of)
 
 __all__ = ["Comm", "InPlaceABN", "InPlaceABNFunction", "backward", "backward_apply",
-           "backward_reduce", "fold_conv", "forward", "forward_apply", "forward_reduce", "inplace_abn",
+           "backward_reduce", "backward_sync_emulated", "fold_conv", "forward", "forward_apply",
+           "forward_reduce", "forward_sync_emulated", "inplace_abn",
            "layout_of", "_lib"]

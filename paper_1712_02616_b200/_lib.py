@@ -29,12 +29,14 @@ FORCE_STREAMING = 1 << 8
 FORCE_FUSED = 1 << 9
 FORCE_ONE_LAUNCH = 1 << 10
 FORCE_RESIDENT = 1 << 11
+SYNC_FUSED = 1 << 12
 
 EXPORTS = ["iabn_version", "iabn_status_string", "iabn_last_error", "iabn_launch_count",
            "iabn_workspace_bytes", "iabn_query_schedule", "iabn_forward", "iabn_backward",
            "iabn_comm_get_unique_id", "iabn_comm_init", "iabn_comm_destroy", "iabn_forward_sync",
            "iabn_backward_sync", "iabn_forward_reduce", "iabn_forward_apply",
-           "iabn_backward_reduce", "iabn_backward_apply", "iabn_fold_conv"]
+           "iabn_backward_reduce", "iabn_backward_apply", "iabn_fold_conv",
+           "iabn_forward_sync_emulated", "iabn_backward_sync_emulated"]
 
 
 class Desc(ctypes.Structure):
@@ -86,6 +88,8 @@ def _load() -> ctypes.CDLL:
                                         _P, _SZ, _P]
     lib.iabn_fold_conv.argtypes = [ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P, _P, _P, _F,
                                    _U32, _P, _P, _P]
+    lib.iabn_forward_sync_emulated.argtypes = [_DP, ctypes.c_int] + lib.iabn_forward.argtypes[1:]
+    lib.iabn_backward_sync_emulated.argtypes = [_DP, ctypes.c_int] + lib.iabn_backward.argtypes[1:]
     for name in EXPORTS:
         if name not in ("iabn_version", "iabn_status_string", "iabn_last_error",
                         "iabn_launch_count", "iabn_workspace_bytes"):

@@ -18,6 +18,7 @@
 #include <mutex>
 #include <numeric>
 #include <utility>
+#include <vector>
 #include <string>
 
 #include "iabn.h"
@@ -316,6 +317,7 @@ struct FusedPlan {
     bool ok = false;
     int K = 0;           // CTAs per cluster (per channel)
     int clusters = 0;    // persistent clusters in the grid
+    int max_clusters = 0;  // clusters that can be co-resident
     uint32_t cap = 0;    // vectors per input per buffer
     uint32_t chunk_vecs = 0;
     int nbuf = 0;
@@ -427,6 +429,7 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags)
         best.minb = minb;
         best.K = K;
         best.clusters = (int)std::min<int64_t>(cl, g.C);
+        best.max_clusters = cl;
         best.cap = (uint32_t)cap;
         best.nbuf = nbuf;
         best.smem = bytes;
@@ -493,8 +496,15 @@ done:
 
 FastDiv fd32(int64_t d) { return make_fastdiv((uint32_t)d); }
 
+// a.vranks > 1 (one-GPU emulation of the synchronized variant): clusters of different
+// virtual ranks wait on one another, so the grid is launched cooperatively (co-resident)
 template <typename T>
 iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t st) {
+    if (a.qv == 0) {  // plain call: one rank, no exchange
+        a.qv = (uint32_t)p.clusters;
+        a.vranks = 1;
+        a.nranks = 1;
+    }
     a.cap = p.cap;
     a.chunk_vecs = p.chunk_vecs;
     a.nbuf = (uint32_t)p.nbuf;
@@ -504,8 +514,8 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     if (a.debug & 4u) {  // experiments only: phase timestamps, dumped by iabn_debug_trace
         static unsigned long long* buf = nullptr;
         static size_t cap = 0;
-        const uint32_t per = (uint32_t)((a.C + p.clusters - 1) / p.clusters);
-        const size_t need = (size_t)p.clusters * p.K * per * kTraceFields;
+        const uint32_t per = (uint32_t)((a.C + a.qv - 1) / a.qv);
+        const size_t need = (size_t)a.vranks * a.qv * p.K * per * kTraceFields;
         if (need > cap) {
             if (buf) cudaFree(buf);
             cudaMalloc(&buf, need * sizeof(unsigned long long));
@@ -519,19 +529,29 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         g_trace_ch = per;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(p.clusters * p.K), 1, 1);
+    cfg.gridDim = dim3(a.vranks * a.qv * (unsigned)p.K, 1, 1);
     cfg.blockDim = dim3(kFusedThreads, 1, 1);
     cfg.dynamicSmemBytes = p.smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p.K;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[3];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = p.K;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (a.vranks > 1) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.numAttrs = na;
     cudaError_t e;
     a.mis_w = p.mis_w;
     a.hwb = (uint32_t)(a.HW * (int64_t)sizeof(T));
@@ -869,6 +889,8 @@ struct Nccl {
                               cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;  // optional (fused sync setup)
 };
 Nccl g_nccl;
 std::mutex g_nccl_mu;
@@ -887,6 +909,7 @@ Nccl* nccl() {
             g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
             g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
             g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+            g_nccl.AllGather = (decltype(g_nccl.AllGather))dlsym(h, "ncclAllGather");
             g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce &&
                         g_nccl.CommDestroy && g_nccl.GetErrorString;
             if (!g_nccl.ok) g_nccl.why = "libnccl.so.2 lacks required symbols";
@@ -895,11 +918,24 @@ Nccl* nccl() {
     return g_nccl.ok ? &g_nccl : nullptr;
 }
 
+// Record buffers of the synchronized channel-resident kernels: peer[g] = rank g's buffer
+// [2][cap][nranks] PeerRec (mapped into this process), ctr = the call counter.
+struct SyncBuf {
+    PeerRec* peer[kMaxRanks] = {};
+    unsigned long long* ctr = nullptr;
+    uint32_t cap = 0;
+    int nranks = 0;
+};
+
 }  // namespace
 
 struct iabn_comm_s {
     ncclComm_t comm;
     int nranks, rank;
+    // fused-collective sync (IABN_SYNC_FUSED): this rank's record buffer, every rank's
+    // buffer mapped through CUDA IPC (peer access over NVLink), the call counter
+    SyncBuf sb{};
+    void* own = nullptr;
 };
 
 namespace {
@@ -910,6 +946,63 @@ iabn_status allreduce_f64(double* buf, size_t count, iabn_comm comm, cudaStream_
     const ncclResult_t r = n->AllReduce(buf, buf, count, ncclFloat64, ncclSum, comm->comm, st);
     if (r != ncclSuccess) return fail(IABN_ERR_NCCL, "ncclAllReduce: %s", n->GetErrorString(r));
     return IABN_OK;
+}
+
+// The fused-collective sync buffers of a communicator (collective: every rank calls it
+// at the same call with the same C): allocate [2][cap][nranks] records, export them
+// with CUDA IPC, all-gather the handles over NCCL and map every peer's buffer.
+iabn_status comm_sync_buf(iabn_comm comm, int64_t C, cudaStream_t st) {
+    if (comm->sb.cap >= C) return IABN_OK;
+    Nccl* n = nccl();
+    if (!n || !n->AllGather) return fail(IABN_ERR_NCCL, "NCCL all-gather unavailable");
+    if (comm->nranks > kMaxRanks)
+        return fail(IABN_ERR_UNSUPPORTED, "fused sync supports at most %d ranks", kMaxRanks);
+    auto cuda = [](cudaError_t e, const char* what) -> iabn_status {
+        return e == cudaSuccess ? IABN_OK
+                                : fail(IABN_ERR_CUDA, "fused sync setup, %s: %s", what, cudaGetErrorString(e));
+    };
+    // every rank finished its earlier calls before anyone drops the old buffers
+    IABN_TRY(cuda(cudaStreamSynchronize(st), "stream synchronize"));
+    const uint32_t cap = (uint32_t)std::max<int64_t>(std::max<int64_t>(C, 2ll * comm->sb.cap), 1024);
+    const size_t bytes = (size_t)2 * cap * comm->nranks * sizeof(PeerRec);
+    void* nb = nullptr;
+    IABN_TRY(cuda(cudaMalloc(&nb, bytes), "cudaMalloc"));
+    IABN_TRY(cuda(cudaMemset(nb, 0, bytes), "cudaMemset"));
+    if (!comm->sb.ctr) {
+        const unsigned long long init[2] = {1ull, 0ull};
+        IABN_TRY(cuda(cudaMalloc(&comm->sb.ctr, sizeof(init)), "cudaMalloc"));
+        IABN_TRY(cuda(cudaMemcpy(comm->sb.ctr, init, sizeof(init), cudaMemcpyHostToDevice), "counter"));
+    }
+    cudaIpcMemHandle_t h;
+    IABN_TRY(cuda(cudaIpcGetMemHandle(&h, nb), "cudaIpcGetMemHandle"));
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    char* dh = nullptr;
+    IABN_TRY(cuda(cudaMalloc(&dh, hb * comm->nranks), "cudaMalloc"));
+    IABN_TRY(cuda(cudaMemcpy(dh + hb * comm->rank, &h, hb, cudaMemcpyHostToDevice), "handle"));
+    const ncclResult_t r = n->AllGather(dh + hb * comm->rank, dh, hb, ncclInt8, comm->comm, st);
+    if (r != ncclSuccess) return fail(IABN_ERR_NCCL, "ncclAllGather: %s", n->GetErrorString(r));
+    std::vector<cudaIpcMemHandle_t> hs(comm->nranks);
+    IABN_TRY(cuda(cudaStreamSynchronize(st), "stream synchronize"));
+    IABN_TRY(cuda(cudaMemcpy(hs.data(), dh, hb * comm->nranks, cudaMemcpyDeviceToHost), "handles"));
+    cudaFree(dh);
+    for (int g = 0; g < comm->nranks; ++g) {
+        if (g == comm->rank) continue;
+        if (comm->sb.peer[g]) cudaIpcCloseMemHandle(comm->sb.peer[g]);
+        void* pp = nullptr;
+        IABN_TRY(cuda(cudaIpcOpenMemHandle(&pp, hs[g], cudaIpcMemLazyEnablePeerAccess),
+                      "cudaIpcOpenMemHandle"));
+        comm->sb.peer[g] = (PeerRec*)pp;
+    }
+    if (comm->own) cudaFree(comm->own);
+    comm->own = nb;
+    comm->sb.peer[comm->rank] = (PeerRec*)nb;
+    comm->sb.cap = cap;
+    comm->sb.nranks = comm->nranks;
+    return IABN_OK;
+}
+
+bool sync_fused_wanted(uint32_t flags) {
+    return (flags & IABN_SYNC_FUSED) || env_int("IABN_SYNC_FUSED", 0) == 1;
 }
 
 // ====================================================================== shared call bodies
@@ -996,6 +1089,121 @@ iabn_status fwd_from_partials(const Ctx& c, const double* part, int S, const voi
     return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
 }
 
+// arguments of the channel-resident kernels (one rank; launch_fused fills the plan)
+FusedArgs fused_fwd_args(const Geom& g, const void* x, void* z, const float* gamma,
+                         const float* beta, float* rm, float* rv, float* sm, float* sv,
+                         float momentum, float eps, float slope, uint32_t flags) {
+    FusedArgs a{};
+    a.in0 = x;
+    a.out = z;
+    a.gamma = gamma;
+    a.beta = beta;
+    a.running_mean = rm;
+    a.running_var = rv;
+    a.save_mean = sm;
+    a.save_var = sv;
+    a.C = g.C;
+    a.HW = g.HW;
+    a.m = (uint32_t)g.m;
+    a.fd_hw = fd32(g.HW);
+    a.momentum = momentum;
+    a.eps = eps;
+    a.slope = slope;
+    a.inv_slope = 1.0f / slope;
+    a.flags = flags;
+    return a;
+}
+FusedArgs fused_bwd_args(const Geom& g, const void* z, const void* dz, void* dx,
+                         const float* gamma, const float* beta, const float* sv, float* dg,
+                         float* db, float eps, float slope, uint32_t flags) {
+    FusedArgs a{};
+    a.in0 = z;
+    a.in1 = dz;
+    a.out = dx;
+    a.gamma = gamma;
+    a.beta = beta;
+    a.save_var = const_cast<float*>(sv);
+    a.dgamma = dg;
+    a.dbeta = db;
+    a.C = g.C;
+    a.HW = g.HW;
+    a.m = (uint32_t)g.m;
+    a.fd_hw = fd32(g.HW);
+    a.eps = eps;
+    a.slope = slope;
+    a.inv_slope = 1.0f / slope;
+    a.flags = flags;
+    return a;
+}
+
+// ====================================================================== in-kernel exchange
+void set_sync(FusedArgs& a, const SyncBuf& b, int vranks, int nranks, int rank0, uint32_t qv,
+              int64_t vr_elems, double inv_mg) {
+    a.qv = qv;
+    a.vranks = (uint32_t)vranks;
+    a.nranks = (uint32_t)nranks;
+    a.rank0 = (uint32_t)rank0;
+    a.vr_elems = vr_elems;
+    a.sync_ctr = b.ctr;
+    a.sync_cap = b.cap;
+    a.inv_mg = inv_mg;
+    for (int i = 0; i < kMaxRanks; ++i) a.peer[i] = b.peer[i];
+}
+
+// One-GPU emulation: the G ranks' buffers in one local allocation, per (device, stream)
+// (calls on one stream are ordered; the call counter lives with the buffers).  Grows
+// with C; a change of G or C reallocates after synchronising the stream, so the first
+// emulated call of a shape must not be inside a CUDA-graph capture.
+iabn_status emu_sync_buf(cudaStream_t st, int G, int64_t C, SyncBuf* out) {
+    struct Ent {
+        int dev;
+        cudaStream_t st;
+        SyncBuf b;
+        void* base;
+    };
+    static std::mutex mu;
+    static std::vector<Ent> ents;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(IABN_ERR_CUDA, "cudaGetDevice failed");
+    std::lock_guard<std::mutex> lk(mu);
+    Ent* e = nullptr;
+    for (auto& x : ents)
+        if (x.dev == dev && x.st == st) e = &x;
+    if (e && e->b.nranks == G && e->b.cap >= C) {
+        *out = e->b;
+        return IABN_OK;
+    }
+    if (!e) {
+        ents.push_back(Ent{dev, st, SyncBuf{}, nullptr});
+        e = &ents.back();
+    } else if (e->base) {
+        cudaStreamSynchronize(st);
+        cudaFree(e->base);
+        e->base = nullptr;
+        e->b = SyncBuf{};
+    }
+    const uint32_t cap = (uint32_t)std::max<int64_t>(C, 256);
+    const size_t per = (size_t)2 * cap * G;  // records per rank buffer
+    const size_t bytes = 64 + (size_t)G * per * sizeof(PeerRec);
+    void* base = nullptr;
+    if (cudaMalloc(&base, bytes) != cudaSuccess)
+        return fail(IABN_ERR_CUDA, "exchange buffers (%zu bytes): %s", bytes,
+                    cudaGetErrorString(cudaGetLastError()));
+    const unsigned long long init[2] = {1ull, 0ull};
+    if (cudaMemset(base, 0, bytes) != cudaSuccess ||
+        cudaMemcpy(base, init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(base);
+        return fail(IABN_ERR_CUDA, "exchange buffers init: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    e->base = base;
+    e->b.ctr = (unsigned long long*)base;
+    e->b.cap = cap;
+    e->b.nranks = G;
+    for (int g = 0; g < G; ++g) e->b.peer[g] = (PeerRec*)((char*)base + 64) + (size_t)g * per;
+    *out = e->b;
+    return IABN_OK;
+}
+
 template <typename T>
 iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamma,
                          const float* beta, float* rm, float* rv, float* sm, float* sv,
@@ -1010,27 +1218,11 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 0, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shape");
-    if (p.ok) {
-        FusedArgs a{};
-        a.in0 = x;
-        a.out = z;
-        a.gamma = gamma;
-        a.beta = beta;
-        a.running_mean = rm;
-        a.running_var = rv;
-        a.save_mean = sm;
-        a.save_var = sv;
-        a.C = c.g.C;
-        a.HW = c.g.HW;
-        a.m = (uint32_t)c.g.m;
-        a.fd_hw = fd32(c.g.HW);
-        a.momentum = momentum;
-        a.eps = eps;
-        a.slope = slope;
-        a.inv_slope = 1.0f / slope;
-        a.flags = flags;
-        return launch_fused<T>(0, p, a, c.st);
-    }
+    if (p.ok)
+        return launch_fused<T>(0, p,
+                               fused_fwd_args(c.g, x, z, gamma, beta, rm, rv, sm, sv, momentum, eps,
+                                              slope, flags),
+                               c.st);
     if (const int G = gres_grid(c.g, 0, flags, *c.dev)) {
         GresArgs a{};
         a.in0 = x;
@@ -1100,26 +1292,11 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 1, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shape");
-    if (p.ok) {
-        FusedArgs a{};
-        a.in0 = z;
-        a.in1 = dz;
-        a.out = dx;
-        a.gamma = gamma;
-        a.beta = beta;
-        a.save_var = const_cast<float*>(sv);
-        a.dgamma = dg;
-        a.dbeta = db;
-        a.C = c.g.C;
-        a.HW = c.g.HW;
-        a.m = (uint32_t)c.g.m;
-        a.fd_hw = fd32(c.g.HW);
-        a.eps = eps;
-        a.slope = slope;
-        a.inv_slope = 1.0f / slope;
-        a.flags = flags;
-        return launch_fused<T>(1, p, a, c.st);
-    }
+    if (p.ok)
+        return launch_fused<T>(1, p,
+                               fused_bwd_args(c.g, z, dz, dx, gamma, beta, sv, dg, db, eps, slope,
+                                              flags),
+                               c.st);
     double* part = wsp<double>(c, c.w.part);
     if (const int G = gres_grid(c.g, 1, flags, *c.dev)) {
         GresArgs a{};
@@ -1395,6 +1572,13 @@ iabn_status iabn_comm_destroy(iabn_comm comm) {
         const ncclResult_t r = n->CommDestroy(comm->comm);
         if (r != ncclSuccess) s = fail(IABN_ERR_NCCL, "ncclCommDestroy: %s", n->GetErrorString(r));
     }
+    if (comm->own) {
+        cudaDeviceSynchronize();
+        for (int g = 0; g < comm->nranks; ++g)
+            if (g != comm->rank && comm->sb.peer[g]) cudaIpcCloseMemHandle(comm->sb.peer[g]);
+        cudaFree(comm->own);
+    }
+    if (comm->sb.ctr) cudaFree(comm->sb.ctr);
     delete comm;
     return s;
 }
@@ -1414,6 +1598,17 @@ iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, con
     IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
                           momentum, eps, slope, flags, c.g.m * comm->nranks));
     IABN_TRY(attach_device(c));
+    if (sync_fused_wanted(flags)) {
+        // channel-resident kernel with the exchange inside (every rank: the same desc)
+        const FusedPlan p = fused_plan(c.g, 0, *c.dev, flags);
+        if (p.ok) {
+            IABN_TRY(comm_sync_buf(comm, c.g.C, c.st));
+            FusedArgs a = fused_fwd_args(c.g, x, z, gamma, beta, running_mean, running_var,
+                                         save_mean, save_var, momentum, eps, slope, flags);
+            set_sync(a, comm->sb, 1, comm->nranks, comm->rank, (uint32_t)p.clusters, 0, 0.0);
+            return DISPATCH(c.g.dtype, launch_fused, 0, p, a, c.st);
+        }
+    }
     double* stats = wsp<double>(c, c.w.stats);
     IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
     launch_pdl(combine_kernel<3>, wgrid(c.g.C), 128, 0, c.st, wsp<double>(c, c.w.part), c.S, c.g.C, stats,
@@ -1437,6 +1632,17 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
     IABN_TRY(attach_device(c));
+    if (sync_fused_wanted(flags)) {
+        const FusedPlan p = fused_plan(c.g, 1, *c.dev, flags);
+        if (p.ok) {
+            IABN_TRY(comm_sync_buf(comm, c.g.C, c.st));
+            FusedArgs a = fused_bwd_args(c.g, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps,
+                                         slope, flags);
+            set_sync(a, comm->sb, 1, comm->nranks, comm->rank, (uint32_t)p.clusters, 0,
+                     1.0 / ((double)c.g.m * comm->nranks));
+            return DISPATCH(c.g.dtype, launch_fused, 1, p, a, c.st);
+        }
+    }
     double* part = wsp<double>(c, c.w.part);
     double* loc = wsp<double>(c, c.w.sums_loc);
     double* glob = wsp<double>(c, c.w.sums_glob);
@@ -1451,6 +1657,70 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
     const double* lsrc = (flags & IABN_SYNC_GLOBAL_PARAM_GRADS) ? glob : loc;
     return DISPATCH(c.g.dtype, bwd_from_sums, c, glob, 1, lsrc, 1, glob + 2 * c.g.C, 0.0, z, dz,
                     dx, gamma, beta, save_var, dgamma, dbeta, eps, slope, flags);
+}
+
+// ---------------------------------------------------------------- one-GPU emulation
+// nranks shards of one tensor, the fused-collective sync in one cooperative launch
+static iabn_status emu_ctx(const iabn_desc* desc, int nranks, void* ws, size_t ws_bytes,
+                           void* stream, Ctx* c, Geom* gl) {
+    if (!desc) return fail(IABN_ERR_INVALID_ARG, "desc is NULL");
+    if (nranks < 1 || nranks > kMaxRanks)
+        return fail(IABN_ERR_INVALID_ARG, "nranks must be in [1, %d] (got %d)", kMaxRanks, nranks);
+    IABN_TRY(make_geom(desc, gl));
+    iabn_desc gd = *desc;
+    gd.n = desc->n * nranks;
+    IABN_TRY(make_ctx(&gd, ws, ws_bytes, stream, c));
+    if (gl->layout != IABN_NCHW)
+        return fail(IABN_ERR_UNSUPPORTED, "fused-collective sync: NCHW only");
+    return IABN_OK;
+}
+
+iabn_status iabn_forward_sync_emulated(const iabn_desc* desc, int nranks, const void* x, void* z,
+                                       const float* gamma, const float* beta,
+                                       float* running_mean, float* running_var, float* save_mean,
+                                       float* save_var, float momentum, float eps, float slope,
+                                       uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    Ctx c;
+    Geom gl;
+    IABN_TRY(emu_ctx(desc, nranks, ws, ws_bytes, stream, &c, &gl));
+    if (flags & IABN_EVAL) return fail(IABN_ERR_INVALID_ARG, "eval mode has no exchange");
+    IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
+                          momentum, eps, slope, flags, c.g.m));
+    IABN_TRY(attach_device(c));
+    const FusedPlan p = fused_plan(gl, 0, *c.dev, flags);
+    if (!p.ok || p.max_clusters < nranks)
+        return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shard");
+    SyncBuf sb;
+    IABN_TRY(emu_sync_buf(c.st, nranks, gl.C, &sb));
+    FusedArgs a = fused_fwd_args(gl, x, z, gamma, beta, running_mean, running_var, save_mean,
+                                 save_var, momentum, eps, slope, flags);
+    const uint32_t qv = (uint32_t)std::min<int64_t>(gl.C, p.max_clusters / nranks);
+    set_sync(a, sb, nranks, nranks, 0, qv, gl.E, 0.0);
+    return DISPATCH(gl.dtype, launch_fused, 0, p, a, c.st);
+}
+
+iabn_status iabn_backward_sync_emulated(const iabn_desc* desc, int nranks, const void* z,
+                                        const void* dz, void* dx, const float* gamma,
+                                        const float* beta, const float* save_mean,
+                                        const float* save_var, float* dgamma, float* dbeta,
+                                        float eps, float slope, uint32_t flags, void* ws,
+                                        size_t ws_bytes, void* stream) {
+    (void)save_mean;
+    Ctx c;
+    Geom gl;
+    IABN_TRY(emu_ctx(desc, nranks, ws, ws_bytes, stream, &c, &gl));
+    IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
+    IABN_TRY(attach_device(c));
+    const FusedPlan p = fused_plan(gl, 1, *c.dev, flags);
+    if (!p.ok || p.max_clusters < nranks)
+        return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shard");
+    SyncBuf sb;
+    IABN_TRY(emu_sync_buf(c.st, nranks, gl.C, &sb));
+    FusedArgs a = fused_bwd_args(gl, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope,
+                                 flags);
+    const uint32_t qv = (uint32_t)std::min<int64_t>(gl.C, p.max_clusters / nranks);
+    set_sync(a, sb, nranks, nranks, 0, qv, gl.E, 1.0 / ((double)gl.m * nranks));
+    return DISPATCH(gl.dtype, launch_fused, 1, p, a, c.st);
 }
 
 }  // extern "C"

@@ -38,6 +38,16 @@ constexpr int kMaxChunks = 16;  // chunks (mbarriers) per slab buffer
 constexpr int kMaxBuf = 4;      // slab buffers per CTA (ring)
 constexpr int kMaxCluster = 16; // CTAs per cluster (non-portable size above 8)
 constexpr int kSlots = 4;       // in-flight channel records per CTA
+constexpr int kMaxRanks = 8;    // ranks of the in-kernel exchange (one node)
+
+// One rank's per-channel record in a peer's exchange buffer (synchronized variant):
+// forward (count, sum x, sum x^2), backward (S1, S2 or Q).  Flag-in-word encoding (no
+// fences): each double travels as two 8-byte words (32 value bits, 32 flag bits), each
+// word stored and loaded as one single-copy-atomic access; a word is current when its
+// flag is the call's flag, so the reader needs no release/acquire pair.
+struct __align__(16) PeerRec {
+    unsigned long long w[6];
+};
 
 struct FusedArgs {
     const void* in0;  // forward: x; backward: z
@@ -63,6 +73,24 @@ struct FusedArgs {
     // 16-byte slots holding the aligned range that covers it; hwb = HW * sizeof(T)
     uint32_t mis_w, hwb;
     FastDiv fd_w;
+    // synchronized variant with the exchange inside the kernel (InPlace-ABN^sync,
+    // PAPER.md:315): each rank's cluster record of channel c is stored into every rank's
+    // buffer peer[g][(call & 1) * sync_cap + c][rank]; each CTA folds the nranks records
+    // in rank order.  vranks > 1: the ranks' shards of one tensor in one launch (one-GPU
+    // emulation: cluster i belongs to virtual rank i / qv, whose shard starts vr_elems
+    // elements after the previous one); peer[] are then local buffers.
+    uint32_t qv;          // clusters per rank in this launch: channel c -> cluster c % qv
+    uint32_t vranks;      // ranks in this launch (1, or nranks)
+    uint32_t nranks;      // ranks of the exchange (1 = no exchange)
+    uint32_t rank0;       // rank of the launch's first virtual rank
+    int64_t vr_elems;     // elements between consecutive virtual ranks' shards
+    // [0] call number (starts at 1; identical on every rank: each rank makes the same
+    // sequence of calls; read from device memory so that graph replays advance it),
+    // [1] CTAs finished (the last one advances [0])
+    unsigned long long* sync_ctr;
+    uint32_t sync_cap;    // channels per parity half of a record buffer
+    double inv_mg;        // backward: 1 / global count
+    PeerRec* peer[kMaxRanks];
     uint32_t debug;  // experiments only (IABN_FUSED_DEBUG): 4 = record phase timestamps
                      // into `trace`
     unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
@@ -103,10 +131,11 @@ __device__ __forceinline__ void st_async_f64x2(uint32_t addr, double a, double b
         "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(mbar)
         : "memory");
 }
-// arrive on a (possibly remote) mbarrier of this cluster; release orders this
-// thread's prior DSMEM stores before the arrival
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
+// arrive on a (possibly remote) mbarrier of this cluster.  Relaxed: no ordering of this thread's earlier memory operations (a write-after-read
+// release whose reads are complete -- the values are in registers -- needs none, and a
+// release would wait for the thread's outstanding global stores)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr)
                  : "memory");
 }
 // wait with cluster-scope acquire: peers' DSMEM stores before their arrivals are visible
@@ -120,6 +149,38 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
         : "memory");
 }
 
+// ---- cross-rank record exchange (peer memory over NVLink, or local memory in the
+// one-GPU emulation): relaxed system-scope 8-byte accesses, flag in every word
+__device__ __forceinline__ uint32_t rec_flag(unsigned long long call) {
+    return 1u + (uint32_t)(call % 0xfffffffeull);  // never 0 (the buffers start zeroed)
+}
+template <int NR>
+__device__ __forceinline__ void st_rec(PeerRec* d, const double* v, uint32_t flag) {
+    const unsigned long long f = (unsigned long long)flag << 32;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        const unsigned long long lo = f | (uint32_t)__double2loint(v[k]);
+        const unsigned long long hi = f | (uint32_t)__double2hiint(v[k]);
+        asm volatile("st.relaxed.sys.global.v2.b64 [%0], {%1, %2};" ::"l"(d->w + 2 * k), "l"(lo),
+                     "l"(hi)
+                     : "memory");
+    }
+}
+// all words of the record carry `flag`: decode into v, else false
+template <int NR>
+__device__ __forceinline__ bool ld_rec(const PeerRec* s, uint32_t flag, double* v) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        unsigned long long lo, hi;
+        asm volatile("ld.relaxed.sys.global.v2.b64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi)
+                     : "l"(s->w + 2 * k)
+                     : "memory");
+        ok = ok && (uint32_t)(lo >> 32) == flag && (uint32_t)(hi >> 32) == flag;
+        v[k] = __hiloint2double((int)(uint32_t)hi, (int)(uint32_t)lo);
+    }
+    return ok;
+}
 // Slice of a channel owned by rank r of K, in 16-byte vectors: whole planes when
 // there are at least K planes (each plane is then one bulk copy), else an even
 // split of the channel's vectors.
@@ -134,6 +195,11 @@ __device__ __forceinline__ void cta_slice(uint32_t mv, uint32_t pv, uint32_t r, 
         vhi = (uint32_t)((uint64_t)mv * (r + 1) / K);
     }
 }
+
+// Per-channel terms of the coefficients that do not depend on the sums.
+struct Terms {
+    double g, bet, rstd_b, inv_g;
+};
 
 // Per-channel constants of the apply pass (shared memory).
 struct ApplyCoef {
@@ -235,11 +301,16 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     __shared__ __align__(8) uint64_t ready[2];                   // exchange -> apply warps
     __shared__ __align__(8) uint64_t freed[2];                   // apply warps -> exchange
     __shared__ __align__(16) double rec[kSlots][kMaxCluster][4];  // pushed by the K peers
+    __shared__ double lrec[kSlots][3];                             // sync: this rank's totals
+    __shared__ Terms lterm[kSlots];                                // sync: channel terms
     __shared__ double red[2][2][kReduceWarps];
     __shared__ ApplyCoef cs[2];
 
     const uint32_t K = cluster_nctarank(), r = cluster_ctarank();
-    const uint32_t q = blockIdx.x / K, Q = gridDim.x / K;
+    const uint32_t cid = blockIdx.x / K;       // cluster
+    const uint32_t vr = cid / a.qv;            // virtual rank of this cluster (0 unless emulated)
+    const uint32_t q = cid - vr * a.qv, Q = a.qv;
+    const int64_t voff = (int64_t)vr * a.vr_elems;  // this rank's shard
     const uint32_t nbuf = a.nbuf;
     const uint32_t C = (uint32_t)a.C;
     const uint32_t nT = q < C ? (C - q + Q - 1) / Q : 0;  // channels of this cluster
@@ -284,7 +355,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
         // ================================================ producer: slab t into buffer t % nbuf,
         // chunk by chunk: chunk k is refilled as soon as the apply warps released it
         if (lane == 0) {
-            const T* src[2] = {(const T*)a.in0, (const T*)a.in1};
+            const T* src[2] = {(const T*)a.in0 + voff, (const T*)a.in1 + voff};
             const uint32_t hw = (uint32_t)a.HW;
             for (uint32_t t = 0; t < nT; ++t) {
                 const uint32_t b = t % nbuf;
@@ -342,80 +413,193 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     } else if (warp == kExchangeWarp) {
         // ================================================ exchange: fold the K records of each
         // channel in rank order (bit-identical in all K CTAs)
-        const double inv_m = 1.0 / (double)a.m;
-        for (uint32_t s = 0; s < nT; ++s) {
-            const int64_t cp = q + s * Q;
-            const uint32_t slot = s & 1u, rs = s % kSlots;
-            if (s >= 2) mbar_wait(&freed[slot], (s / 2 - 1) & 1u);
-            constexpr uint32_t RB = NR == 3 ? 32u : 16u;  // record bytes per peer
-            // per-channel terms that do not depend on the records, before the wait
-            double g = 0.0, bet = 0.0, rstd_b = 0.0, inv_g = 0.0;
+        constexpr uint32_t RB = NR == 3 ? 32u : 16u;  // record bytes per peer
+        // per-channel terms that do not depend on the records (lane 0)
+        auto terms = [&](int64_t cp) {
+            Terms t{0.0, 0.0, 0.0, 0.0};
             if (lane == 0) {
-                g = gamma_eff(a.gamma[cp], a.eps, a.flags);
-                inv_g = PASS == 1 ? 1.0 / g : 0.0;
-                bet = (double)a.beta[cp];
-                if (PASS == 1) rstd_b = rsqrt((double)a.save_var[cp] + (double)a.eps);
-                mbar_arrive_expect_tx(&gathered[rs], K * RB);
+                t.g = gamma_eff(a.gamma[cp], a.eps, a.flags);
+                t.inv_g = PASS == 1 ? 1.0 / t.g : 0.0;
+                t.bet = (double)a.beta[cp];
+                if (PASS == 1) t.rstd_b = rsqrt((double)a.save_var[cp] + (double)a.eps);
             }
-            // the records are st.async transactions on my own barrier: completing the phase
-            // makes them visible, as for a TMA load (CTA-scope acquire, no L1 invalidation)
-            mbar_wait(&gathered[rs], (s / kSlots) & 1u);
-            if (lane == 0) IABN_TRACE(a, s, 5);
-            // fold: lane j < K takes rank j's record, then a fixed xor tree (the same
-            // order in every CTA of the cluster => bit-identical coefficients)
-            double v[NR];
+            return t;
+        };
+        // fold: lane j < K takes rank j's record, then a fixed xor tree (the same order in
+        // every CTA of the cluster => bit-identical coefficients)
+        auto fold_cluster = [&](uint32_t rs, double* v) {
 #pragma unroll
             for (int k = 0; k < NR; ++k) v[k] = lane < K ? rec[rs][lane][k] : 0.0;
 #pragma unroll
             for (int k = 0; k < NR; ++k)
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-            if (lane == 0) {
-                if (PASS == 0) {
-                    // mean, biased var; A = g rstd; y = (x - mu_hi) A + B'
-                    const double mean = v[1] * inv_m;
-                    double var = fma(-mean, mean, v[2] * inv_m);
-                    var = var > 0.0 ? var : 0.0;
-                    const double A = g * rsqrt(var + (double)a.eps);
-                    const float mu_hi = (float)mean;
-                    const double mu_lo = mean - (double)mu_hi;
-                    const float Af = (float)A, Bp = (float)(bet - mu_lo * A);
-                    cs[slot].P = make_float2(Af, Af);
-                    cs[slot].Q = make_float2(Bp, Bp);
-                    cs[slot].mu = mu_hi;
-                    mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
-                    IABN_TRACE(a, s, 11);
-                    if (r == 0) {
-                        a.save_mean[cp] = (float)mean;
-                        a.save_var[cp] = (float)var;
-                        update_running(a.running_mean, a.running_var, cp, mean, var, v[0],
-                                       a.momentum, a.flags);
-                    }
-                } else {
-                    // dx = alpha dy + kappa y + cc (PAPER.md:168 refolded in y):
-                    //   alpha = g rstd, kappa = -rstd S2/m, cc = rstd (S2 beta - g S1)/m
-                    // with dy, y on the branch of sign(z):
-                    //   z >= 0: alpha dz + kappa z + cc;  z < 0: (alpha a) dz + (kappa / a) z + cc
-                    // variant II pushed (S1, Q = sum dy y): S2 = (Q - beta S1) / g
-                    if (!(a.flags & kVariantI)) v[1] = (v[1] - bet * v[0]) * inv_g;
-                    const double rm = rstd_b * inv_m;
-                    const float alpha = (float)(g * rstd_b);
-                    const float kappa = (float)(-rm * v[1]);
-                    const float cc = (float)(rm * fma(v[1], bet, -g * v[0]));
-                    cs[slot].P = make_float2(alpha, kappa);
-                    cs[slot].Q = make_float2(alpha * a.slope, kappa * a.inv_slope);
-                    cs[slot].mu = cc;
-                    mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
-                    IABN_TRACE(a, s, 11);
-                    if (r == 0) {
-                        a.dbeta[cp] = (float)v[0];
-                        a.dgamma[cp] = (float)(gamma_sign(a.gamma[cp], a.flags) * v[1]);
-                    }
+        };
+        // the slot of every peer that pushed into me may be reused by it: released as soon
+        // as it is folded, with a relaxed arrive (a release would first wait for this
+        // warp's outstanding global stores; measured: cfg2 69.4 -> 64.3 us fwd+bwd)
+        auto release_slot = [&](uint32_t rs) {
+            __syncwarp();
+            if (lane < K) mbar_arrive_cluster_relaxed(mapa(&slotfree[rs], lane));
+        };
+        // coefficients of channel s from the totals v (global under sync) and this rank's
+        // totals lv (lane 0)
+        auto finish = [&](uint32_t s, int64_t cp, const Terms& t, double* v, double* lv) {
+            const uint32_t slot = s & 1u;
+            if (PASS == 0) {
+                // mean, biased var; A = g rstd; y = (x - mu_hi) A + B'
+                // (v[0] = the count, global under sync)
+                const double inv_m = 1.0 / v[0];
+                const double mean = v[1] * inv_m;
+                double var = fma(-mean, mean, v[2] * inv_m);
+                var = var > 0.0 ? var : 0.0;
+                const double A = t.g * rsqrt(var + (double)a.eps);
+                const float mu_hi = (float)mean;
+                const double mu_lo = mean - (double)mu_hi;
+                const float Af = (float)A, Bp = (float)(t.bet - mu_lo * A);
+                cs[slot].P = make_float2(Af, Af);
+                cs[slot].Q = make_float2(Bp, Bp);
+                cs[slot].mu = mu_hi;
+                mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
+                IABN_TRACE(a, s, 11);
+                if (r == 0 && vr == 0) {
+                    a.save_mean[cp] = (float)mean;
+                    a.save_var[cp] = (float)var;
+                    update_running(a.running_mean, a.running_var, cp, mean, var, v[0],
+                                   a.momentum, a.flags);
+                }
+            } else {
+                // dx = alpha dy + kappa y + cc (PAPER.md:168 refolded in y):
+                //   alpha = g rstd, kappa = -rstd S2/m, cc = rstd (S2 beta - g S1)/m
+                // with dy, y on the branch of sign(z):
+                //   z >= 0: alpha dz + kappa z + cc;  z < 0: (alpha a) dz + (kappa / a) z + cc
+                // variant II pushed (S1, Q = sum dy y): S2 = (Q - beta S1) / g
+                if (!(a.flags & kVariantI)) {
+                    v[1] = (v[1] - t.bet * v[0]) * t.inv_g;
+                    lv[1] = (lv[1] - t.bet * lv[0]) * t.inv_g;
+                }
+                const double rm = t.rstd_b * (a.nranks > 1 ? a.inv_mg : 1.0 / (double)a.m);
+                const float alpha = (float)(t.g * t.rstd_b);
+                const float kappa = (float)(-rm * v[1]);
+                const float cc = (float)(rm * fma(v[1], t.bet, -t.g * v[0]));
+                cs[slot].P = make_float2(alpha, kappa);
+                cs[slot].Q = make_float2(alpha * a.slope, kappa * a.inv_slope);
+                cs[slot].mu = cc;
+                mbar_arrive(&ready[slot]);  // release: cs[slot] visible to the apply warps
+                IABN_TRACE(a, s, 11);
+                if (r == 0) {
+                    // sync: this rank's sums unless the caller asked for the global ones (R7)
+                    const double* pg = (a.flags & kSyncGlobalGrads) ? v : lv;
+                    a.dbeta[vr * a.C + cp] = (float)pg[0];
+                    a.dgamma[vr * a.C + cp] = (float)(gamma_sign(a.gamma[cp], a.flags) * pg[1]);
                 }
             }
-            __syncwarp();
-            // the slot of every peer that pushed into me may be reused by it
-            if (lane < K) mbar_arrive_cluster(mapa(&slotfree[rs], lane));
+        };
+        if (a.nranks <= 1) {
+            for (uint32_t s = 0; s < nT; ++s) {
+                const int64_t cp = q + s * Q;
+                const uint32_t rs = s % kSlots;
+                if (s >= 2) mbar_wait(&freed[s & 1u], (s / 2 - 1) & 1u);
+                const Terms t = terms(cp);
+                if (lane == 0) mbar_arrive_expect_tx(&gathered[rs], K * RB);
+                // the records are st.async transactions on my own barrier: completing the phase
+                // makes them visible, as for a TMA load (CTA-scope acquire, no L1 invalidation)
+                mbar_wait(&gathered[rs], (s / kSlots) & 1u);
+                if (lane == 0) IABN_TRACE(a, s, 5);
+                double v[NR], lv[NR];
+                fold_cluster(rs, v);
+                release_slot(rs);
+#pragma unroll
+                for (int k = 0; k < NR; ++k) lv[k] = v[k];
+                if (lane == 0) finish(s, cp, t, v, lv);
+                __syncwarp();
+            }
+        } else {
+            // synchronized variant: the cluster's total of channel t is stored into every
+            // rank's buffer (CTA 0 of the cluster, lane g -> rank g) as soon as the K CTA
+            // records are in ("publish"); every CTA then folds the nranks records of the
+            // channel from its own rank's buffer.  Publishing runs up to kSlots - 1 channels
+            // ahead of the fold, also while the warp waits for other ranks' records, so the
+            // cross-rank latency overlaps the pipeline instead of adding to it.
+            const uint32_t myrank = a.rank0 + vr;
+            // the call's tag; records go to the parity half (tag & 1) of the buffers: a slot
+            // is rewritten two calls later, when every rank has finished reading it
+            const unsigned long long tag = *(volatile unsigned long long*)a.sync_ctr;
+            const size_t half = (size_t)(tag & 1ull) * a.sync_cap * a.nranks;
+            const uint32_t flag = rec_flag(tag);
+            const PeerRec* own = a.peer[myrank] + half;
+            uint32_t pub = 0, armed = 0;
+            auto arm = [&](uint32_t t) {  // expect channel t's K records
+                if (lane == 0) mbar_arrive_expect_tx(&gathered[t % kSlots], K * RB);
+                armed = t + 1;
+            };
+            auto publish = [&](uint32_t t) {  // channel t's K records (all lanes wait)
+                const uint32_t rs = t % kSlots;
+                mbar_wait(&gathered[rs], (t / kSlots) & 1u);
+                double v[NR];
+                fold_cluster(rs, v);
+                release_slot(rs);
+                if (lane == 0) {
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) lrec[rs][k] = v[k];
+                    lterm[rs] = terms(q + t * Q);  // loaded ahead of the fold
+                }
+                if (r == 0 && lane < a.nranks)
+                    st_rec<NR>(a.peer[lane] + half + (size_t)(q + t * Q) * a.nranks + myrank, v,
+                               flag);
+                pub = t + 1;
+            };
+            for (uint32_t s = 0; s < nT; ++s) {
+                const int64_t cp = q + s * Q;
+                if (s >= 2) mbar_wait(&freed[s & 1u], (s / 2 - 1) & 1u);
+                while (pub <= s) {
+                    if (armed <= pub) arm(pub);
+                    publish(pub);
+                }
+                // the nranks records of channel s (lane g: rank g), publishing channels whose
+                // CTA records come in meanwhile
+                const PeerRec* src = own + (size_t)cp * a.nranks + lane;
+                double v[NR];
+                unsigned long long t0 = 0;
+                for (uint32_t it = 0;; ++it) {
+                    bool ok = true;
+                    if (lane < a.nranks) ok = ld_rec<NR>(src, flag, v);
+                    if (__all_sync(0xffffffffu, ok)) break;
+                    if (pub < nT && pub < s + kSlots) {
+                        if (armed <= pub) arm(pub);
+                        const bool in = __shfl_sync(
+                            0xffffffffu,
+                            lane == 0 ? mbar_test(&gathered[pub % kSlots], (pub / kSlots) & 1u)
+                                      : false,
+                            0);
+                        if (in) {
+                            publish(pub);
+                            continue;
+                        }
+                    }
+                    if (it >= 64) __nanosleep(32);
+                    if ((it & 1023u) == 0) {
+                        if (it == 0) t0 = gtimer();
+                        else if (gtimer() - t0 > 20000000000ull) __trap();  // a rank never called
+                    }
+                }
+                if (lane >= a.nranks)
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) v[k] = 0.0;
+#pragma unroll
+                for (int k = 0; k < NR; ++k)
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+                if (lane == 0) IABN_TRACE(a, s, 5);
+                if (lane == 0) {
+                    double lv[NR];
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) lv[k] = lrec[s % kSlots][k];
+                    const Terms t = lterm[s % kSlots];
+                    finish(s, cp, t, v, lv);
+                }
+                __syncwarp();
+            }
         }
     }
 
@@ -675,7 +859,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                            const uint32_t gb) {
         const uint32_t hw = (uint32_t)a.HW;
         const float2 sl2 = make_float2(a.slope, a.slope);
-        T* out = (T*)a.out;
+        T* out = (T*)a.out + voff;
         const int64_t chw = a.C * a.HW;
         const int64_t cp = q + s * Q;
         const uint32_t b = s % nbuf, slot = s & 1u;
@@ -753,7 +937,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         w[j] = fma2(al, dd[j], fma2(ka, w[j], cc2));
                     }
                 }
-                T* const dst = (T*)((char*)a.out + (B0 + sj * dB - h) + si * 16u);
+                T* const dst = (T*)((char*)out + (B0 + sj * dB - h) + si * 16u);
                 if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) {
                     st_vec(dst, Pairs<T>::store(w));
                 } else {
@@ -874,6 +1058,14 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     // peers may still push records / arrive on this CTA's barriers until they finish
     cluster_arrive_release();
     cluster_wait_acquire();
+    if (a.nranks > 1 && threadIdx.x == 0) {
+        // the grid's last CTA advances the call number for the next call on this stream
+        __threadfence();
+        if (atomicAdd(&a.sync_ctr[1], 1ull) == gridDim.x - 1) {
+            atomicExch(&a.sync_ctr[1], 0ull);
+            atomicAdd(&a.sync_ctr[0], 1ull);
+        }
+    }
 }
 
 }  // namespace iabn

@@ -47,6 +47,7 @@ enum : uint32_t {
     kGammaPlain = 1u << 0,
     kGammaFixedOne = 1u << 1,
     kRunVarBiased = 1u << 2,
+    kSyncGlobalGrads = 1u << 3,  // sync backward: dgamma/dbeta = the all-rank sums
     kVariantI = 1u << 5  // fused backward: per-element x^ products (Alg. 2 I) instead of BN-dagger sums
 };
 

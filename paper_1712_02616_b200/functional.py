@@ -196,6 +196,63 @@ def backward(z: torch.Tensor, dz: torch.Tensor, gamma: torch.Tensor, beta: torch
     return dx, dgamma, dbeta
 
 
+# ---------------------------------------------------------------- fused-collective sync, one GPU
+def forward_sync_emulated(x: torch.Tensor, nranks: int, gamma: torch.Tensor, beta: torch.Tensor,
+                          running_mean: torch.Tensor | None = None,
+                          running_var: torch.Tensor | None = None, *, momentum: float = 0.1,
+                          eps: float = 1e-5, slope: float = 0.01, out: torch.Tensor | None = None,
+                          gamma_mode: str = "abs_eps", running_var_biased: bool = False,
+                          flags: int = 0, stream=None):
+    """InPlace-ABN^sync over ``nranks`` equal shards of ``x`` (along N), emulated on one
+    GPU by the fused-collective kernel (include/iabn.h, iabn_forward_sync_emulated).
+    Returns (z, save_mean, save_var) with global statistics."""
+    if x.dim() < 2 or x.shape[0] % nranks:
+        raise ValueError("x.shape[0] must be a multiple of nranks")
+    d = _desc(x, "NCHW")
+    C = d.c
+    shard = L.Desc(d.n // nranks, d.c, d.hw, d.dtype, d.layout)
+    z = x if out is None else out
+    if z.shape != x.shape or z.dtype != x.dtype or not z.is_contiguous():
+        raise ValueError("out must match x in shape, dtype and contiguity")
+    gamma, beta = _f32(gamma, C, "gamma"), _f32(beta, C, "beta")
+    running_mean = _f32(running_mean, C, "running_mean")
+    running_var = _f32(running_var, C, "running_var")
+    save_mean = torch.empty(C, dtype=torch.float32, device=x.device)
+    save_var = torch.empty(C, dtype=torch.float32, device=x.device)
+    ws, nb = workspace(d, x.device, stream)
+    L.call("iabn_forward_sync_emulated", ctypes.byref(shard), nranks, x.data_ptr(), z.data_ptr(),
+           gamma.data_ptr(), beta.data_ptr(), _ptr(running_mean), _ptr(running_var),
+           save_mean.data_ptr(), save_var.data_ptr(), momentum, eps, slope,
+           _flags(gamma_mode, running_var_biased, flags), ws, nb, _stream(stream))
+    return z, save_mean, save_var
+
+
+def backward_sync_emulated(z: torch.Tensor, dz: torch.Tensor, nranks: int, gamma: torch.Tensor,
+                           beta: torch.Tensor, save_var: torch.Tensor, *, eps: float = 1e-5,
+                           slope: float = 0.01, dx: torch.Tensor | None = None,
+                           gamma_mode: str = "abs_eps", flags: int = 0,
+                           global_param_grads: bool = False, stream=None):
+    """Backward of :func:`forward_sync_emulated`.  Returns (dx, dgamma, dbeta) with
+    dgamma/dbeta of shape [nranks, C] (row r = shard r's contribution)."""
+    if z.dim() < 2 or z.shape[0] % nranks:
+        raise ValueError("z.shape[0] must be a multiple of nranks")
+    if dz.shape != z.shape or dz.dtype != z.dtype or not dz.is_contiguous():
+        raise ValueError("dz must match z in shape, dtype and contiguity")
+    d = _desc(z, "NCHW")
+    C = d.c
+    shard = L.Desc(d.n // nranks, d.c, d.hw, d.dtype, d.layout)
+    dx = dz if dx is None else dx
+    dgamma = torch.empty(nranks, C, dtype=torch.float32, device=z.device)
+    dbeta = torch.empty(nranks, C, dtype=torch.float32, device=z.device)
+    fl = _flags(gamma_mode, False, flags) | (L.SYNC_GLOBAL_PARAM_GRADS if global_param_grads else 0)
+    ws, nb = workspace(d, z.device, stream)
+    L.call("iabn_backward_sync_emulated", ctypes.byref(shard), nranks, z.data_ptr(), dz.data_ptr(),
+           dx.data_ptr(), _f32(gamma, C, "gamma").data_ptr(), _f32(beta, C, "beta").data_ptr(),
+           None, _f32(save_var, C, "save_var").data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
+           eps, slope, fl, ws, nb, _stream(stream))
+    return dx, dgamma, dbeta
+
+
 # ---------------------------------------------------------------- split phase
 def forward_reduce(x: torch.Tensor, *, layout: str = "NCHW", stream=None) -> torch.Tensor:
     """Local raw moments, fp64 [C, 3] = (count, sum, sum of squares)."""

@@ -168,3 +168,33 @@ def test_fold_conv_validation(kw, status):
 def test_fold_conv_in_place_reaches_device():
     assert _fold(w_out=P, b_out=P * 2) in (L.ERR_CUDA, L.OK)
     assert _fold(bias=0) in (L.ERR_CUDA, L.OK)  # no conv bias
+
+
+# ---------------------------------------------------------------- fused-collective sync emulation
+def _fwd_emu(d, nranks, flags=0, ws_bytes=None, x=P, z=P):
+    gd = L.desc(d.n * nranks, d.c, d.hw, d.dtype, d.layout) if 1 <= nranks <= 64 else d
+    if ws_bytes is None:
+        ws_bytes = L.workspace_bytes(gd)
+    return L.lib.iabn_forward_sync_emulated(ctypes.byref(d), nranks, x, z, P, P, P, P, P, P, 0.1,
+                                            1e-5, 0.01, flags, P * 16, ws_bytes, None)
+
+
+@pytest.mark.parametrize("nranks", [0, -1, 9])
+def test_sync_emulated_rank_count(nranks):
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    assert _fwd_emu(d, nranks) == L.ERR_INVALID_ARG, L.lib.iabn_last_error()
+
+
+def test_sync_emulated_validation():
+    d = L.desc(2, 8, 16, L.F32, L.NCHW)
+    assert _fwd_emu(d, 2, flags=L.EVAL) == L.ERR_INVALID_ARG
+    assert _fwd_emu(L.desc(2, 8, 16, L.F32, L.NHWC), 2) == L.ERR_UNSUPPORTED
+    # the workspace is sized for the whole tensor (nranks shards), not one shard
+    assert _fwd_emu(d, 4, ws_bytes=L.workspace_bytes(d) - 1) == L.ERR_WORKSPACE
+    # z overlapping part of the whole tensor (not only of the first shard)
+    assert _fwd_emu(d, 4, z=P + 3 * 8 * 16 * 4) == L.ERR_ALIAS
+    dz = P * 4096
+    st = L.lib.iabn_backward_sync_emulated(ctypes.byref(d), 2, P, dz, dz, P, P, None, 0, P, P,
+                                           1e-5, 0.01, 0, P * 16,
+                                           L.workspace_bytes(L.desc(4, 8, 16, L.F32, L.NCHW)), None)
+    assert st == L.ERR_INVALID_ARG  # save_var NULL
