@@ -61,6 +61,13 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--schedule", choices=["auto", "streaming", "fused"], default="auto",
                     help="schedule override (IABN_FORCE_*), for experiments")
+    ap.add_argument("--sync", choices=["nccl", "fused"], default="nccl",
+                    help="N > 1: reduce / ncclAllReduce / apply kernels (default), or the "
+                         "fused-collective kernels (IABN_SYNC_FUSED: record exchange over "
+                         "NVLink inside the channel-resident kernels)")
+    ap.add_argument("--sync-emulated", type=int, default=8,
+                    help="N = 1: also time the fused-collective sync over this many virtual "
+                         "ranks on the same workload (one-GPU emulation; 0 = off)")
     return ap.parse_args()
 
 
@@ -307,6 +314,8 @@ def main():
     # keep the repeated in-place application bounded: re-standardise x and dz once
     # outside the timed region if they drift (z of a layer is the next layer's input)
     fl = {"auto": 0, "streaming": L.FORCE_STREAMING, "fused": L.FORCE_FUSED}[args.schedule]
+    if world > 1 and args.sync == "fused":
+        fl |= L.SYNC_FUSED
 
     def step():
         z, sm, sv = P.forward(x, g, bt, rm, rv, comm=comm, flags=fl)
@@ -370,10 +379,11 @@ def main():
     # dominant kernel: the backward (3*E*b algorithmic bytes per launch)
     bwd_ms = bwd_sum / K
     fwd_ms = fwd_sum / K
+    qfl = fl if world == 1 or args.sync == "fused" else L.FORCE_STREAMING
     s_f, k_f = L.query_schedule(L.desc(N_local, C, HW, L.BF16 if b == 2 else L.F32, L.NCHW), 0,
-                                fl if world == 1 else L.FORCE_STREAMING)
+                                qfl)
     s_b, k_b = L.query_schedule(L.desc(N_local, C, HW, L.BF16 if b == 2 else L.F32, L.NCHW), 1,
-                                fl if world == 1 else L.FORCE_STREAMING)
+                                qfl)
     bwd_bytes = 3 * E * b
     achieved = bwd_bytes / (bwd_ms * 1e-3) / 1e9
     traffic = load_traffic(args.config) if world == 1 else None
@@ -470,6 +480,42 @@ def main():
             allreduce[name] = {"bytes": n * 8, "us": round(tt.item(), 2),
                                "pct_of_step": round(100 * tt.item() * 1e-3 / ms_per_step, 2)}
 
+    # synchronized variant on one GPU: the fused-collective kernels over G virtual ranks
+    # (the G shards of this workload, records exchanged through the peer-record protocol)
+    sync_emu = None
+    G = args.sync_emulated
+    if world == 1 and G > 1 and wl["N"] % G == 0 and wl["layout"] == "NCHW":
+        def emu_step():
+            z, _, sv = P.forward_sync_emulated(x, G, g, bt, rm, rv)
+            P.backward_sync_emulated(z, dz, G, g, bt, sv)
+            return sv
+        for _ in range(3):
+            emu_step()
+        torch.cuda.synchronize()
+        ne = max(1, min(args.steps, 50))
+        fe, be = [], []
+        for _ in range(ne):
+            if flush is not None:
+                flush.add_(1.0)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(st)
+            z, _, sv = P.forward_sync_emulated(x, G, g, bt, rm, rv)
+            e1.record(st)
+            P.backward_sync_emulated(z, dz, G, g, bt, sv)
+            e2.record(st)
+            torch.cuda.synchronize()
+            fe.append(e0.elapsed_time(e1))
+            be.append(e1.elapsed_time(e2))
+        ems = (sum(fe) + sum(be)) / ne
+        ev_ = bytes_step_all / (ems * 1e-3) / 1e9
+        sync_emu = {"virtual_ranks": G, "N_per_rank": wl["N"] // G, "value": round(ev_, 2),
+                    "unit": "GB/s", "pct_of_peak": round(100 * ev_ / peak, 2),
+                    "ms_per_step": round(ems, 4), "fwd_ms": round(sum(fe) / ne, 4),
+                    "bwd_ms": round(sum(be) / ne, 4), "steps": ne,
+                    "path": "iabn_forward_sync_emulated + iabn_backward_sync_emulated: one "
+                            "cooperative launch per pass, G ranks' channel records exchanged "
+                            "in-kernel (no NCCL launch); 5*E*b bytes"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(wl, args.cpu_seconds)
@@ -482,7 +528,7 @@ def main():
             "dtype": wl["dtype"], "data": "synthetic",
             "config": {"workload": f"{args.config}: {wl['desc']}", "global_batch": wl["N"],
                        "N_local": N_local, "C": C, "HW": HW, "layout": wl["layout"],
-                       "parallelism": f"dp{world}" + ("+sync-stats" if world > 1 else ""),
+                       "parallelism": f"dp{world}" + (f"+sync-stats({args.sync})" if world > 1 else ""),
                        "l2": ("inputs larger than L2 (x, dz %.2f GB each)" % (E * b / 1e9))
                        if flush is None else "L2 flushed before every timed step",
                        "schedule": {"forward": SCHEDULES[s_f] + (f" K={k_f}" if s_f == 1 else ""),
@@ -507,6 +553,8 @@ def main():
             line["clocks_rejected_first_run"] = rejected
         if allreduce:
             line["allreduce"] = allreduce
+        if sync_emu:
+            line["sync_emulated"] = sync_emu
         print(json.dumps(line), flush=True)
 
     if comm is not None:

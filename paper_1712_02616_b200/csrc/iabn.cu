@@ -482,6 +482,18 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags)
             if (consider(K, 1)) goto done;
     }
 done:
+    // small slabs: more of them in flight per CTA when they fit in the same budget (the
+    // per-channel latency -- load, record exchange, coefficients -- is then hidden by more
+    // channels in flight rather than by bigger ones)
+    if (best.ok && best.nbuf == 2 && !env_int("IABN_FUSED_NBUF", 0) &&
+        env_int("IABN_FUSED_DEEP", 1)) {
+        const FusedPlan keep = best;
+        const int K = best.K;
+        int nb = kMaxBuf;
+        for (; nb > 2; --nb)
+            if (consider(K, nb) && best.clusters == keep.clusters) break;
+        if (nb == 2) best = keep;
+    }
     if (best.ok && env_int("IABN_VERBOSE", 0)) {
         static std::mutex pm;
         static int printed = 0;
