@@ -718,7 +718,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 if constexpr (MIS) {
                     // slot v of the slice = (plane jn, slot i) with v = jn W + i; a cursor
                     // steps it by RT (no division in the loop); the plane's head offset
-                    // is h0 + jn dh (mod 16); kMRU slots' shared loads issued first
+                    // is h0 + jn dh (mod 16); kMRU slots' shared loads issued first.  The
+                    // main loop takes the interior slots only; the (at most two) partial
+                    // slots of each plane follow in a loop of their own, one per thread
+                    // (in the main loop they would make every warp run the masked path)
                     constexpr int kMRU = MINB == 4 ? 2 : 4;
                     const uint32_t W = a.mis_w, n0 = vlo / W;
                     const uint32_t h0 = mis_plane((uint64_t)n0 * a.C + c, a.hwb).h;
@@ -726,10 +729,21 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     const uint32_t qp = RT / W, qr = RT % W;
                     auto one = [&](const uint4 zu, const uint4 du, uint32_t si, uint32_t sj) {
                         const uint32_t h = (h0 + sj * dh) & 15u;
-                        if (si * 16u >= h && si * 16u + 16u <= h + a.hwb)
-                            reduce_vec(zu, du, v2tag);
-                        else if (si * 16u < h + a.hwb)
-                            reduce_vec_masked(zu, du, si, h, v2tag);
+                        if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) reduce_vec(zu, du, v2tag);
+                    };
+                    // partial slots of planes [p_lo, p_hi): e = 2 (plane - p_lo) + {0 head, 1 tail}
+                    auto edges = [&](uint32_t p_lo, uint32_t p_hi) {
+                        for (uint32_t e = tid; e < 2u * (p_hi - p_lo); e += RT) {
+                            const uint32_t jn = p_lo + (e >> 1);
+                            const uint32_t h = (h0 + jn * dh) & 15u;
+                            const uint32_t tail = (h + a.hwb - 1u) >> 4;
+                            const uint32_t si = (e & 1u) ? tail : 0u;
+                            if ((e & 1u) && tail == 0u) continue;  // one slot: the head's
+                            if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) continue;  // interior
+                            const uint32_t v = jn * W + si;
+                            const uint4 zu = lds128(xs + v * 16u);
+                            reduce_vec_masked(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, si, h, v2tag);
+                        }
                     };
                     for (int k = 0; k < nch; ++k) {
                         if (PASS == 1 || k > 0) group_wait(&full[b][k], par, gw == 0, gb, RT);
@@ -769,6 +783,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                                 ++jn;
                             }
                         }
+                        edges(c_lo / W, c_hi / W);
                     }
                 } else {
                     for (int k = 0; k < nch; ++k) {
@@ -904,17 +919,19 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
         };
         if constexpr (MIS) {
             // slots of the slice by a stride cursor (as in the reduce); interior slots are
-            // whole 16-byte stores, the (at most two) edge slots of a plane store only its
-            // own elements (the rest of those 16 bytes belong to neighbouring channels)
+            // whole 16-byte stores; the (at most two) edge slots of a plane store only its
+            // own elements (the rest of those 16 bytes belong to neighbouring channels),
+            // in a loop of their own after the interior ones (as in the reduce)
             constexpr int kMAU = MINB == 4 ? 2 : 4;
             const uint32_t W = a.mis_w, n0 = vlo / W;
             const uint64_t B0 = ((uint64_t)n0 * a.C + cp) * a.hwb;  // plane 0's first byte
             const uint64_t dB = (uint64_t)a.C * a.hwb;               // bytes between planes
             const uint32_t h0 = (uint32_t)(B0 & 15u), dh = (uint32_t)(dB & 15u);
             const uint32_t qp = AT / W, qr = AT % W;
-            auto one = [&](const uint4 xu, const uint4 du, uint32_t si, uint32_t sj) {
+            auto one = [&](const uint4 xu, const uint4 du, uint32_t si, uint32_t sj, bool edge) {
                 const uint32_t h = (h0 + sj * dh) & 15u;
-                if (si * 16u >= h + a.hwb) return;  // slot beyond the plane's cover
+                const bool interior = si * 16u >= h && si * 16u + 16u <= h + a.hwb;
+                if (interior == edge) return;  // main loop: interior slots; edge loop: the rest
                 float2 w[NP];
                 if (PASS == 0) {
                     Pairs<T>::load_sub(xu, mu, w);
@@ -938,7 +955,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     }
                 }
                 T* const dst = (T*)((char*)out + (B0 + sj * dB - h) + si * 16u);
-                if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) {
+                if (!edge) {
                     st_vec(dst, Pairs<T>::store(w));
                 } else {
 #pragma unroll
@@ -969,11 +986,11 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         }
                     }
 #pragma unroll
-                    for (int q = 0; q < kMAU; ++q) one(xu[q], du[q], iu[q], ju[q]);
+                    for (int q = 0; q < kMAU; ++q) one(xu[q], du[q], iu[q], ju[q], false);
                 }
                 for (; v < c_hi;) {
                     const uint4 xu = lds128(xs + v * 16u);
-                    one(xu, PASS == 1 ? lds128(ds + v * 16u) : xu, i, jn);
+                    one(xu, PASS == 1 ? lds128(ds + v * 16u) : xu, i, jn, false);
                     v += AT;
                     i += qr;
                     jn += qp;
@@ -981,6 +998,18 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         i -= W;
                         ++jn;
                     }
+                }
+                // edge slots: e = 2 (plane - p_lo) + {0 head, 1 tail}
+                const uint32_t p_lo = c_lo / W;
+                for (uint32_t e = at; e < 2u * (c_hi / W - p_lo); e += AT) {
+                    const uint32_t pj = p_lo + (e >> 1);
+                    const uint32_t h = (h0 + pj * dh) & 15u;
+                    const uint32_t tail = (h + a.hwb - 1u) >> 4;
+                    if ((e & 1u) && tail == 0u) continue;  // one slot: the head's
+                    const uint32_t si = (e & 1u) ? tail : 0u;
+                    const uint32_t vv = pj * W + si;
+                    const uint4 xu = lds128(xs + vv * 16u);
+                    one(xu, PASS == 1 ? lds128(ds + vv * 16u) : xu, si, pj, true);
                 }
                 __syncwarp();
                 if ((at & 31) == 0) mbar_arrive(&empty[b][k]);

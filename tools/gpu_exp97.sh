@@ -1,0 +1,12 @@
+# whole-network sweeps with per-shape device times from per-shape CUDA graphs
+for cfg in "rx101 bf16 NCHW" "rx101 f32 NCHW" "densenet264 bf16 NCHW"; do
+  set -- $cfg
+  timeout 600 python tools/sweep.py --net $1 --dtype $2 --layout $3 > gpurun_out/sw_$1_$2_$3.json 2> gpurun_out/sw_$1_$2_$3.err
+  python - gpurun_out/sw_$1_$2_$3.json <<'PY'
+import json, sys
+d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+print(d["net"], d["dtype"], d["layout"], "graph", d["graph_ms"], "ms", d["graph_pct_of_peak"], "%")
+for r in sorted(d["per_shape"], key=lambda r: -r["share_pct"])[:12]:
+    print("   ", r)
+PY
+done

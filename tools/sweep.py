@@ -127,25 +127,24 @@ def main():
         sequence()
     t_graph = timed(graph.replay, args.reps)
 
-    # per-shape device time: each layer alone, events around its fwd / bwd
+    # per-shape device time: for each distinct shape, the forwards of all its layers (in
+    # network order, each on its own buffers) captured in one CUDA graph, the backwards in
+    # another; replayed, device time per layer (launch gaps excluded as in the sequence)
     per = OrderedDict()
-    st = torch.cuda.current_stream().cuda_stream
-    evs = []
-    for i in range(len(layers)):
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        e[0].record()
-        run_fwd(i, st)
-        e[1].record()
-        run_bwd(i, st)
-        e[2].record()
-        evs.append(e)
-    torch.cuda.synchronize()
-    for (C, HW), e in zip(layers, evs):
-        k = f"{C}x{HW}"
-        r = per.setdefault(k, dict(C=C, HW=HW, count=0, fwd_us=0.0, bwd_us=0.0))
-        r["count"] += 1
-        r["fwd_us"] += e[0].elapsed_time(e[1]) * 1e3
-        r["bwd_us"] += e[1].elapsed_time(e[2]) * 1e3
+    for i, (C, HW) in enumerate(layers):
+        per.setdefault(f"{C}x{HW}", dict(C=C, HW=HW, idx=[]))["idx"].append(i)
+    for k, r in per.items():
+        r["count"] = len(r["idx"])
+        for name, fn in (("fwd_us", run_fwd), ("bwd_us", run_bwd)):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                for i in r["idx"]:
+                    fn(i, s.cuda_stream)  # warm-up on the capture stream
+            torch.cuda.synchronize()
+            with torch.cuda.graph(gr, stream=s):
+                for i in r["idx"]:
+                    fn(i, s.cuda_stream)
+            r[name] = timed(gr.replay, max(args.reps, 5)) * 1e3
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     shapes = []
     for k, r in per.items():
@@ -153,6 +152,7 @@ def main():
         t = (r["fwd_us"] + r["bwd_us"]) * 1e-6
         shapes.append(dict(shape=k, count=r["count"], fwd_us=round(r["fwd_us"] / r["count"], 2),
                            bwd_us=round(r["bwd_us"] / r["count"], 2),
+                           share_pct=round(100 * (r["fwd_us"] + r["bwd_us"]) * 1e-3 / t_graph, 1),
                            pct_of_peak=round(100 * 5 * e * b / t / 1e9 / peak, 1)))
     res = dict(net=args.net, dtype=args.dtype, layout=args.layout, N=N, layers=len(layers),
                elements=E, algorithmic_bytes=5 * E * b, out_of_place=out_of_place,

@@ -51,6 +51,13 @@ def report(tr, label, grid_ch):
         "apply (apply0->applyN)": tr[..., 7] - tr[..., 6],
         "residence (issue0->applyN)": tr[..., 7] - tr[..., 0],
     }
+    first = np.where(valid[:, 0], tr[:, 0, 0], 0)
+    last = tr[..., 7].max(axis=1)
+    ok = valid[:, 0]
+    print(f"  CTA first issue after t0: p10 {np.percentile((first[ok] - t0) / 1e3, 10):.2f} p50 "
+          f"{np.percentile((first[ok] - t0) / 1e3, 50):.2f} p90 {np.percentile((first[ok] - t0) / 1e3, 90):.2f}"
+          f" max {(first[ok] - t0).max() / 1e3:.2f} us; CTA last store: p50 "
+          f"{np.percentile((last[ok] - t0) / 1e3, 50):.2f} max {(last[ok] - t0).max() / 1e3:.2f} us")
     for k, v in iv.items():
         x = v[valid] / 1e3
         print(f"  {k:32s} p10 {np.percentile(x, 10):7.2f}  p50 {np.percentile(x, 50):7.2f}  "
@@ -63,6 +70,7 @@ def report(tr, label, grid_ch):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="wrn38")
+    ap.add_argument("--shape", default=None, help="N,C,HW,dtype (overrides --config)")
     args = ap.parse_args()
     assert int(os.environ.get("IABN_FUSED_DEBUG", "0")) & 4, "set IABN_FUSED_DEBUG=4"
     import paper_1712_02616_b200 as P
@@ -70,7 +78,11 @@ def main():
     import synth_inputs as S
     L.lib.iabn_debug_trace.restype = ctypes.c_size_t
     L.lib.iabn_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-    cfg = S.CONFIGS[args.config]
+    if args.shape:
+        n_, c_, hw_, dt_ = args.shape.split(",")
+        cfg = dict(N=int(n_), C=int(c_), HW=int(hw_), dtype=dt_)
+    else:
+        cfg = S.CONFIGS[args.config]
     N, C, HW = cfg["N"], cfg["C"], cfg["HW"]
     dev = torch.device("cuda", 0)
     x = S.make_x(N, C, HW, 1, dtype=cfg["dtype"], device=dev)
