@@ -152,3 +152,42 @@ def test_sync_fused_rejects_bad_arguments():
         P.forward_sync_emulated(x, 4, g, b)  # 6 samples do not split into 4 shards
     with pytest.raises(IabnError):
         P.forward_sync_emulated(x.repeat(2, 1, 1)[:9 * 1], 9, g, b)  # more than 8 ranks
+
+
+@pytest.mark.slow
+def test_sync_fused_full_size_sampled_channels():
+    """bench.py's workload (WideResNet-38 16x4096x112x112 bf16) as 8 virtual ranks of 2
+    crops (the launch configuration of its `sync_emulated` figure): sampled whole channels
+    against the oracle on the full batch, every channel's dbeta against sum(dy) from z."""
+    import numpy as np
+    import paper_1712_02616_b200 as P
+    import synth_inputs as S
+    cfg = S.CONFIGS["wrn38"]
+    N, C, HW, G = cfg["N"], cfg["C"], cfg["HW"], 8
+    x = S.make_x(N, C, HW, 0, dtype="bf16")
+    dz = S.make_dz(N, C, HW, 0, dtype="bf16")
+    p = S.make_params(C, 0)
+    g, b = p.gamma.cuda(), p.beta.cuda()
+    rm, rv = p.running_mean.cuda(), p.running_var.cuda()
+    z, sm, sv = P.forward_sync_emulated(x.cuda(), G, g, b, rm, rv)
+    dzd = dz.cuda()
+    dx, dg, db = P.backward_sync_emulated(z, dzd, G, g, b, sv, dx=torch.empty_like(dzd))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(7)
+    ch = torch.tensor(sorted({0, C - 1, *rng.choice(C, 10, replace=False).tolist()}))
+    sub = Case(N, len(ch), HW, dtype="bf16")
+    ps = S.Params(p.gamma[ch], p.beta[ch], p.running_mean[ch], p.running_var[ch])
+    chd = ch.cuda()
+    got = dict(z=z[:, chd, :].cpu(), dx=dx[:, chd, :].cpu(), mean=sm[chd].cpu(),
+               var=sv[chd].cpu(), rm=rm[chd].cpu(), rv=rv[chd].cpu(),
+               dgamma=dg[:, chd].sum(0).cpu(), dbeta=db[:, chd].sum(0).cpu())
+    compare(sub, got, run_oracle(sub, x[:, ch, :].contiguous(), dz[:, ch, :].contiguous(), ps), ps)
+    zf = z.double()
+    dy = torch.where(zf >= 0, dzd.double(), dzd.double() * 0.01)
+    ref = dy.sum(dim=(0, 2))
+    assert ((db.double().sum(0) - ref).abs().max() / ref.abs().max()).item() < 1e-3
+    # each virtual rank's row is its own shard's sum
+    n = N // G
+    for r in (0, G - 1):
+        refr = dy[r * n:(r + 1) * n].sum(dim=(0, 2))
+        assert ((db[r].double() - refr).abs().max() / refr.abs().max()).item() < 1e-3
