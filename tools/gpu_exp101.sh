@@ -1,0 +1,9 @@
+# TMEM staging (IABN_FUSED_TMEM=1): parity and cfg4 timing
+IABN_FUSED_TMEM=1 IABN_VERBOSE=1 timeout 120 python -m pytest tests/test_parity_gpu.py -x -q -p no:cacheprovider -k "cfg1 or fused_and_streaming or deterministic or large_planes or backward_variants" 2>&1 | tail -4
+B="python bench.py --steps 30 --e2e-steps 0 --no-cpu-baseline --sync-emulated 0"
+run() { echo "$1 :: $(env $2 timeout 120 $B 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["fwd_ms"], d["bwd_ms"], d["pct_of_peak"])')"; }
+run default "X=1"
+run "tmem" "IABN_FUSED_TMEM=1"
+run "tmem K8" "IABN_FUSED_TMEM=1 IABN_FUSED_K=8"
+run "tmem K8 nb1" "IABN_FUSED_TMEM=1 IABN_FUSED_K=8 IABN_FUSED_NBUF=1"
+IABN_FUSED_TMEM=1 IABN_VERBOSE=1 timeout 120 $B 2>&1 | grep "\[iabn\]" | sort | uniq | head
