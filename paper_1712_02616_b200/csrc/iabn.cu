@@ -181,6 +181,10 @@ int stat_splits(const Geom& g) {
     }
     int64_t S = (target + units - 1) / units;
     S = std::min<int64_t>(S, std::max<int64_t>(1, work / per_unit_min));
+    // small NHWC layers: at least one CTA per SM when the rows allow >= 32 each (the
+    // reduction is a chain of load latencies per CTA; measured on DenseNet-264 NHWC)
+    if (g.layout == IABN_NHWC && units * S < 148)
+        S = std::max<int64_t>(S, std::min<int64_t>((148 + units - 1) / units, work / 32));
     S = std::max<int64_t>(1, std::min<int64_t>(S, 65535));
     return (int)S;
 }

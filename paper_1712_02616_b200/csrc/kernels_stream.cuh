@@ -41,6 +41,10 @@ constexpr int kUnroll = IABN_STREAM_UNROLL;  // independent 16-byte loads in fli
 #define IABN_STAT_UNROLL 8
 #endif
 constexpr int kStatUnroll = IABN_STAT_UNROLL;  // statistics kernel (one input)
+#ifndef IABN_NHWC_UNROLL
+#define IABN_NHWC_UNROLL 4
+#endif
+constexpr int kNhwcUnroll = IABN_NHWC_UNROLL;  // NHWC reductions: rows in flight per thread
 
 // Gamma reparametrisation (R4).
 enum : uint32_t {
@@ -248,9 +252,11 @@ __device__ __forceinline__ void stats_nhwc_body(const T* __restrict__ x, int64_t
     float a1[V], a2[V];
 #pragma unroll
     for (int k = 0; k < V; ++k) a1[k] = a2[k] = 0.f;
-    double d1[V], d2[V];
+    // fp64 accumulators of this thread in its own slots of red (not registers: the
+    // registers go to loads in flight)
+    double* const d1 = &red[ty][tx * V][0];
 #pragma unroll
-    for (int k = 0; k < V; ++k) d1[k] = d2[k] = 0.0;
+    for (int k = 0; k < V; ++k) d1[2 * k] = d1[2 * k + 1] = 0.0;
     if (active) {
         int iter = 0;
         auto acc = [&](const float (&f)[V]) {
@@ -264,20 +270,20 @@ __device__ __forceinline__ void stats_nhwc_body(const T* __restrict__ x, int64_t
         auto flush = [&]() {
 #pragma unroll
             for (int k = 0; k < V; ++k) {
-                d1[k] += a1[k];
-                d2[k] += a2[k];
+                d1[2 * k] += a1[k];
+                d1[2 * k + 1] += a2[k];
                 a1[k] = a2[k] = 0.f;
             }
         };
         int64_t r0 = rlo + ty;
         if constexpr (VEC) {
-            // raw loads of kStatUnroll rows first (all in range), then the math
-            for (; r0 + 16 * (kStatUnroll - 1) < rhi; r0 += 16 * kStatUnroll) {
-                uint4 raw[kStatUnroll];
+            // raw loads of kNhwcUnroll rows first (all in range), then the math
+            for (; r0 + 16 * (kNhwcUnroll - 1) < rhi; r0 += 16 * kNhwcUnroll) {
+                uint4 raw[kNhwcUnroll];
 #pragma unroll
-                for (int u = 0; u < kStatUnroll; ++u) raw[u] = ld_vec_ro(x + (r0 + 16 * u) * C + c0);
+                for (int u = 0; u < kNhwcUnroll; ++u) raw[u] = ld_vec_ro(x + (r0 + 16 * u) * C + c0);
 #pragma unroll
-                for (int u = 0; u < kStatUnroll; ++u) {
+                for (int u = 0; u < kNhwcUnroll; ++u) {
                     float f[V];
                     unpack<T>(raw[u], f);
                     acc(f);
@@ -304,8 +310,8 @@ __device__ __forceinline__ void stats_nhwc_body(const T* __restrict__ x, int64_t
     }
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-        red[ty][tx * V + k][0] = d1[k] + a1[k];
-        red[ty][tx * V + k][1] = d2[k] + a2[k];
+        d1[2 * k] += a1[k];
+        d1[2 * k + 1] += a2[k];
     }
     __syncthreads();
     const int t = threadIdx.x;
@@ -322,8 +328,14 @@ __device__ __forceinline__ void stats_nhwc_body(const T* __restrict__ x, int64_t
         }
     }
 }
+// NHWC reductions: minimum CTAs per SM for the register allocation (experiments; a
+// cap of 3 or 4 spills in the bf16 kernels and measured slower than none)
+#ifndef IABN_NHWC_MINB
+#define IABN_NHWC_MINB 1
+#endif
+constexpr int kNhwcMinBlocks = IABN_NHWC_MINB;
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kNhwcMinBlocks)
     stats_nhwc_kernel(const T* __restrict__ x, int64_t C, int64_t rows, double* __restrict__ part) {
     pdl_wait();
     stats_nhwc_body<T, VEC>(x, C, rows, part, hw_blk());
@@ -803,17 +815,19 @@ __device__ __forceinline__ void bwd_reduce_nhwc_body(const T* __restrict__ z, co
     const int64_t c0 = (int64_t)bk.x * CT + tx * V;
     const int64_t rlo = rows * s / S, rhi = rows * (s + 1) / S;
     const bool active = c0 < C;
+    constexpr int kBU = kNhwcUnroll / 2 > 0 ? kNhwcUnroll / 2 : 1;  // two inputs per row
     InvAffine ia[V];
 #pragma unroll
     for (int k = 0; k < V; ++k)
         ia[k] = (active && c0 + k < C) ? inv_affine(gamma[c0 + k], beta[c0 + k], eps, flags)
                                        : InvAffine{0.f, 0.f};
     float a1[V], a2[V];
-    double d1[V], d2[V];
+    // fp64 accumulators of this thread in its own slots of red (registers go to loads)
+    double* const d1 = &red[ty][tx * V][0];
 #pragma unroll
     for (int k = 0; k < V; ++k) {
         a1[k] = a2[k] = 0.f;
-        d1[k] = d2[k] = 0.0;
+        d1[2 * k] = d1[2 * k + 1] = 0.0;
     }
     if (active) {
         int iter = 0;
@@ -829,23 +843,23 @@ __device__ __forceinline__ void bwd_reduce_nhwc_body(const T* __restrict__ z, co
         auto flush = [&]() {
 #pragma unroll
             for (int k = 0; k < V; ++k) {
-                d1[k] += a1[k];
-                d2[k] += a2[k];
+                d1[2 * k] += a1[k];
+                d1[2 * k + 1] += a2[k];
                 a1[k] = a2[k] = 0.f;
             }
         };
         int64_t r0 = rlo + ty;
         if constexpr (VEC) {
-            // raw loads of z and dz for kUnroll rows first (all in range), then the math
-            for (; r0 + 16 * (kUnroll - 1) < rhi; r0 += 16 * kUnroll) {
-                uint4 rz[kUnroll], rd[kUnroll];
+            // raw loads of z and dz for kBU rows first (all in range), then the math
+            for (; r0 + 16 * (kBU - 1) < rhi; r0 += 16 * kBU) {
+                uint4 rz[kBU], rd[kBU];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < kBU; ++u) {
                     rz[u] = ld_vec_ro(z + (r0 + 16 * u) * C + c0);
                     rd[u] = ld_vec_ro(dz + (r0 + 16 * u) * C + c0);
                 }
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < kBU; ++u) {
                     float fz[V], fd[V];
                     unpack<T>(rz[u], fz);
                     unpack<T>(rd[u], fd);
@@ -876,8 +890,8 @@ __device__ __forceinline__ void bwd_reduce_nhwc_body(const T* __restrict__ z, co
     }
 #pragma unroll
     for (int k = 0; k < V; ++k) {
-        red[ty][tx * V + k][0] = d1[k] + a1[k];
-        red[ty][tx * V + k][1] = d2[k] + a2[k];
+        d1[2 * k] += a1[k];
+        d1[2 * k + 1] += a2[k];
     }
     __syncthreads();
     const int t = threadIdx.x;
@@ -896,7 +910,7 @@ __device__ __forceinline__ void bwd_reduce_nhwc_body(const T* __restrict__ z, co
     }
 }
 template <typename T, bool VEC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kNhwcMinBlocks)
     bwd_reduce_nhwc_kernel(const T* __restrict__ z, const T* __restrict__ dz,
                            const float* __restrict__ gamma, const float* __restrict__ beta,
                            int64_t C, int64_t rows, float eps, float slope, float inv_slope,
