@@ -5,7 +5,7 @@ IABN_VERBOSE=1 timeout 600 python bench.py > gpurun_out/fin_bench.log 2>&1; echo
 timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/fin_ref.log 2>&1
 timeout 300 python bench.py --config r50s3 --e2e-steps 1 > gpurun_out/fin_r50.log 2>&1
 timeout 300 python bench.py --schedule streaming --steps 100 --e2e-steps 0 --no-cpu-baseline > gpurun_out/fin_stream.log 2>&1
-C="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+C="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --sync-emulated 0"
 timeout 300 $C > gpurun_out/fin_plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/fin_launches.csv $C > gpurun_out/fin_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 2 -c 2 -o gpurun_out/fin_fused $C > gpurun_out/fin_ncu_full.log 2>&1
 IABN_FUSED_DEBUG=4 timeout 300 python tools/trace_fused.py > gpurun_out/fin_trace.log 2>&1
@@ -13,4 +13,10 @@ for cfg in "rx101 f32 NCHW" "rx101 bf16 NCHW" "rx101 f32 NHWC" "densenet264 f32 
   set -- $cfg
   timeout 600 python tools/sweep.py --net $1 --dtype $2 --layout $3 > gpurun_out/fin_sweep_$1_$2_$3.json 2> gpurun_out/fin_sweep_$1_$2_$3.err
 done
-echo done
+echo done1
+for c in wrn38 r50s3 rx101_14; do
+  timeout 300 python tools/sync_emulated.py --cfg $c > gpurun_out/fin_sync_emu_$c.json 2>&1
+done
+timeout 900 python tools/fig4_blocks.py --dtype f32 > gpurun_out/fin_fig4_f32.json 2> gpurun_out/fin_fig4_f32.err
+timeout 900 python tools/fig4_blocks.py --dtype bf16 > gpurun_out/fin_fig4_bf16.json 2> gpurun_out/fin_fig4_bf16.err
+echo done2

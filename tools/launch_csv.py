@@ -16,7 +16,9 @@ def main(path):
     for r in rows:
         lid, name, metric, unit, val = r[0], r[4], r[12], r[13], r[14]
         d = launches.setdefault(int(lid), {"kernel": name[:60]})
-        d[metric] = float(val.replace(",", "")) * UNIT.get(unit, 1)
+        v = float(val.replace(",", "")) if val.replace(",", "").replace(".", "").isdigit() else None
+        if v is not None:
+            d[metric] = v * UNIT.get(unit, 1)
     w = csv.writer(sys.stdout)
     w.writerow(["id", "kernel", "gpu__time_duration_ns", "dram_read_bytes", "dram_write_bytes"])
     for lid in sorted(launches):
