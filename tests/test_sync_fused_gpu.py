@@ -191,3 +191,30 @@ def test_sync_fused_full_size_sampled_channels():
     for r in (0, G - 1):
         refr = dy[r * n:(r + 1) * n].sum(dim=(0, 2))
         assert ((db[r].double() - refr).abs().max() / refr.abs().max()).item() < 1e-3
+
+
+@pytest.mark.parametrize("gamma_mode,flags", [("plain", 0), ("fixed_one", 0), ("abs_eps", 1 << 5),
+                                              ("abs_eps", 1 << 2)],
+                         ids=["gamma_plain", "gamma_fixed_one", "variant_I", "running_var_biased"])
+def test_sync_fused_modes(gamma_mode, flags):
+    """The record exchange under every reparametrisation / variant / running-stat flag."""
+    import paper_1712_02616_b200 as P
+    case = Case(8, 40, 196, dtype="bf16", seed=41, gamma_mode=gamma_mode)
+    x, dz, p = inputs(case)
+    ref = run_oracle(case, x, dz, p)
+    G = 4
+    g, b = p.gamma.cuda(), p.beta.cuda()
+    rm, rv = p.running_mean.cuda(), p.running_var.cuda()
+    kw = dict(eps=case.eps, slope=case.slope, gamma_mode=gamma_mode)
+    z, sm, sv = P.forward_sync_emulated(x.cuda(), G, g, b, rm, rv, momentum=case.momentum,
+                                        running_var_biased=bool(flags & (1 << 2)), **kw)
+    dzd = dz.cuda()
+    dx, dg, db = P.backward_sync_emulated(z, dzd, G, g, b, sv, dx=torch.empty_like(dzd),
+                                          flags=flags & (1 << 5), **kw)
+    torch.cuda.synchronize()
+    got = dict(z=z.cpu(), dx=dx.cpu(), mean=sm.cpu(), var=sv.cpu(), rm=rm.cpu(), rv=rv.cpu(),
+               dgamma=dg.sum(0).cpu(), dbeta=db.sum(0).cpu())
+    if flags & (1 << 2):  # biased running variance: (1 - a) r + a var
+        m = case.momentum
+        ref["rv"] = (1 - m) * to64(p.running_var) + m * ref["var"]
+    compare(case, got, ref, p)

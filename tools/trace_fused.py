@@ -63,6 +63,8 @@ def report(tr, label, grid_ch):
         print(f"  {k:32s} p10 {np.percentile(x, 10):7.2f}  p50 {np.percentile(x, 50):7.2f}  "
               f"p90 {np.percentile(x, 90):7.2f} us")
     step = np.diff(tr[..., 7], axis=1)[valid[:, 1:] & valid[:, :-1]] / 1e3
+    if step.size == 0:  # one channel per CTA
+        return
     print(f"  {'step (applyN(t)->applyN(t+1))':32s} p10 {np.percentile(step, 10):7.2f}  p50 "
           f"{np.percentile(step, 50):7.2f}  p90 {np.percentile(step, 90):7.2f} us")
 
