@@ -91,6 +91,7 @@ struct FusedArgs {
     uint32_t sync_cap;    // channels per parity half of a record buffer
     double inv_mg;        // backward: 1 / global count
     PeerRec* peer[kMaxRanks];
+    uint32_t prefetch;  // L2 prefetch of each slice before its buffer frees up
     uint32_t debug;  // experiments only (IABN_FUSED_DEBUG): 4 = record phase timestamps
                      // into `trace`
     unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
@@ -361,6 +362,36 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 const uint32_t b = t % nbuf;
                 const int64_t c = q + t * Q;
                 uint4* buf = smem + b * bufv;
+                if (a.prefetch && t >= nbuf) {
+                    // the slice's buffer is still being applied: pull the slice into L2 now,
+                    // so that the bulk copies issued as its chunks free up hit L2 (HBM
+                    // latency off the refill path; bytes read from HBM once either way)
+                    if constexpr (MIS) {
+                        for (uint32_t n = vlo / a.mis_w; n < vhi / a.mis_w; ++n) {
+                            const MisPlane mp = mis_plane((uint64_t)n * a.C + c, a.hwb);
+                            const uint32_t nb =
+                                (uint32_t)(((mp.a0 + mp.h + a.hwb + 15) & ~(uint64_t)15) - mp.a0);
+#pragma unroll
+                            for (int i = 0; i < NIN; ++i)
+                                bulk_prefetch_l2((const char*)src[i] + mp.a0, nb);
+                        }
+                    } else {
+                        uint32_t j = vlo * V;
+                        const uint32_t jend = vhi * V;
+                        uint32_t n = fdiv(j, a.fd_hw);
+                        uint32_t sp = j - n * hw;
+                        while (j < jend) {
+                            const uint32_t len = min(jend - j, hw - sp);
+                            const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
+#pragma unroll
+                            for (int i = 0; i < NIN; ++i)
+                                bulk_prefetch_l2(src[i] + goff, len * (uint32_t)sizeof(T));
+                            j += len;
+                            ++n;
+                            sp = 0;
+                        }
+                    }
+                }
                 for (int k = 0; k < nch; ++k) {
                     if (t >= nbuf) {
                         mbar_wait(&empty[b][k], (t / nbuf - 1) & 1u);  // chunk k of t - nbuf applied
