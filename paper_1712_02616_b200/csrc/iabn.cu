@@ -527,7 +527,10 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     // single-buffered slices (the backward of large channels): the refill waits for the
     // apply, so the slice is prefetched into L2 first (cfg4 backward 0.90 -> 0.85 ms;
     // double-buffered kernels measured slightly slower with it)
-    a.prefetch = (uint32_t)env_int("IABN_FUSED_PREFETCH", p.nbuf == 1 ? 1 : 0);
+    {
+        const int pf = env_int("IABN_FUSED_PREFETCH", -1);  // -1 auto, 0 off, 1 on, 2 bwd only
+        a.prefetch = pf < 0 ? (p.nbuf == 1 ? 1u : 0u) : pf == 2 ? (uint32_t)(pass == 1) : (uint32_t)pf;
+    }
     a.debug = (uint32_t)env_int("IABN_FUSED_DEBUG", 0);
     a.trace = nullptr;
     a.trace_ch = 0;
