@@ -530,6 +530,10 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     {
         const int pf = env_int("IABN_FUSED_PREFETCH", -1);  // -1 auto, 0 off, 1 on, 2 bwd only
         a.prefetch = pf < 0 ? (p.nbuf == 1 ? 1u : 0u) : pf == 2 ? (uint32_t)(pass == 1) : (uint32_t)pf;
+        // L2 cache hints: bit 1 = the prefetch marks its lines evict_last (they must survive
+        // until the refill), bit 2 = the refill copies mark them evict_first (used once);
+        // measured: backward 0.848 -> 0.834 ms, DRAM reads 3.45 -> 3.32 GB (3.29 GB minimum)
+        if (a.prefetch) a.prefetch |= (uint32_t)env_int("IABN_FUSED_PF_HINT", 3) << 1;
     }
     a.debug = (uint32_t)env_int("IABN_FUSED_DEBUG", 0);
     a.trace = nullptr;

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
         // chunk by chunk: chunk k is refilled as soon as the apply warps released it
         if (lane == 0) {
             const T* src[2] = {(const T*)a.in0 + voff, (const T*)a.in1 + voff};
+            const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
             const uint32_t hw = (uint32_t)a.HW;
             for (uint32_t t = 0; t < nT; ++t) {
                 const uint32_t b = t % nbuf;
@@ -384,8 +385,13 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                             const uint32_t len = min(jend - j, hw - sp);
                             const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
 #pragma unroll
-                            for (int i = 0; i < NIN; ++i)
-                                bulk_prefetch_l2(src[i] + goff, len * (uint32_t)sizeof(T));
+                            for (int i = 0; i < NIN; ++i) {
+                                if (a.prefetch & 2u)
+                                    bulk_prefetch_l2_hint(src[i] + goff, len * (uint32_t)sizeof(T),
+                                                          pol_last);
+                                else
+                                    bulk_prefetch_l2(src[i] + goff, len * (uint32_t)sizeof(T));
+                            }
                             j += len;
                             ++n;
                             sp = 0;
@@ -430,9 +436,14 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         const uint32_t len = min(jend - j, hw - sp);
                         const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
 #pragma unroll
-                        for (int i = 0; i < NIN; ++i)
-                            bulk_g2s(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
-                                     len * (uint32_t)sizeof(T), &full[b][k]);
+                        for (int i = 0; i < NIN; ++i) {
+                            if ((a.prefetch & 4u) && t >= nbuf)
+                                bulk_g2s_hint(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
+                                              len * (uint32_t)sizeof(T), &full[b][k], pol_first);
+                            else
+                                bulk_g2s(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
+                                         len * (uint32_t)sizeof(T), &full[b][k]);
+                        }
                         j += len;
                         ++n;
                         sp = 0;
