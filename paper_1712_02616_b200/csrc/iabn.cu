@@ -534,6 +534,8 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         // until the refill), bit 2 = the refill copies mark them evict_first (used once);
         // measured: backward 0.848 -> 0.834 ms, DRAM reads 3.45 -> 3.32 GB (3.29 GB minimum)
         if (a.prefetch) a.prefetch |= (uint32_t)env_int("IABN_FUSED_PF_HINT", 3) << 1;
+        // experiments: bit 3 = every bulk copy of the slices evict_first
+        a.prefetch |= (uint32_t)env_int("IABN_FUSED_LOAD_EVICT_FIRST", 0) << 3;
     }
     a.debug = (uint32_t)env_int("IABN_FUSED_DEBUG", 0);
     a.trace = nullptr;

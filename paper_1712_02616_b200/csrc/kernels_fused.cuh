@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 const uint32_t b = t % nbuf;
                 const int64_t c = q + t * Q;
                 uint4* buf = smem + b * bufv;
-                if (a.prefetch && t >= nbuf) {
+                if ((a.prefetch & 1u) && t >= nbuf) {
                     // the slice's buffer is still being applied: pull the slice into L2 now,
                     // so that the bulk copies issued as its chunks free up hit L2 (HBM
                     // latency off the refill path; bytes read from HBM once either way)
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
 #pragma unroll
                         for (int i = 0; i < NIN; ++i) {
-                            if ((a.prefetch & 4u) && t >= nbuf)
+                            if (((a.prefetch & 4u) && t >= nbuf) || (a.prefetch & 8u))
                                 bulk_g2s_hint(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
                                               len * (uint32_t)sizeof(T), &full[b][k], pol_first);
                             else
