@@ -424,6 +424,10 @@ FusedPlan fused_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags)
         // slice: whole planes when N >= K (see cta_slice)
         const bool by_plane = np >= K;
         if (mis && !by_plane) return false;
+        // the small-slab variant only with whole planes per CTA: a plane split across CTAs
+        // (sub-plane chunks, cursor-addressed apply) loses to the 2-CTA/SM variant with
+        // whole planes (fused-collective sync at 2 planes per rank: bwd 1.16 -> 0.97 ms)
+        if (minb == 4 && !by_plane) return false;
         const int64_t cap = by_plane ? pv * ((np + K - 1) / K) : (mv + K - 1) / K;
         const size_t bytes = (size_t)cap * 16 * nin * nbuf;
         if (bytes > lim) return false;
