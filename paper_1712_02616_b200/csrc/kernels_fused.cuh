@@ -356,13 +356,19 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
         // ================================================ producer: slab t into buffer t % nbuf,
         // chunk by chunk: chunk k is refilled as soon as the apply warps released it
         if (lane == 0) {
+            constexpr bool kL2Hints = MINB == 2;
             const T* src[2] = {(const T*)a.in0 + voff, (const T*)a.in1 + voff};
-            const uint64_t pol_last = l2_policy_evict_last(), pol_first = l2_policy_evict_first();
             const uint32_t hw = (uint32_t)a.HW;
             for (uint32_t t = 0; t < nT; ++t) {
                 const uint32_t b = t % nbuf;
                 const int64_t c = q + t * Q;
                 uint4* buf = smem + b * bufv;
+                // one decision per slice (not per copy: the producer lane issues one bulk
+                // copy per plane, ~100 per slice on 14x14 layers)
+                // (L2 hints only in the 2-CTA/SM variant, where single-buffered slices use
+                // them: compiled out of the 4-CTA/SM one, measured ~3 % slower on r50s3 with)
+                const bool hint_first =
+                    kL2Hints && (((a.prefetch & 4u) && t >= nbuf) || (a.prefetch & 8u));
                 if ((a.prefetch & 1u) && t >= nbuf) {
                     // the slice's buffer is still being applied: pull the slice into L2 now,
                     // so that the bulk copies issued as its chunks free up hit L2 (HBM
@@ -386,9 +392,9 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                             const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
 #pragma unroll
                             for (int i = 0; i < NIN; ++i) {
-                                if (a.prefetch & 2u)
+                                if (kL2Hints && (a.prefetch & 2u))
                                     bulk_prefetch_l2_hint(src[i] + goff, len * (uint32_t)sizeof(T),
-                                                          pol_last);
+                                                          l2_policy_evict_last());
                                 else
                                     bulk_prefetch_l2(src[i] + goff, len * (uint32_t)sizeof(T));
                             }
@@ -437,9 +443,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
 #pragma unroll
                         for (int i = 0; i < NIN; ++i) {
-                            if (((a.prefetch & 4u) && t >= nbuf) || (a.prefetch & 8u))
+                            if (hint_first)
                                 bulk_g2s_hint(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
-                                              len * (uint32_t)sizeof(T), &full[b][k], pol_first);
+                                              len * (uint32_t)sizeof(T), &full[b][k],
+                                              l2_policy_evict_first());
                             else
                                 bulk_g2s(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
                                          len * (uint32_t)sizeof(T), &full[b][k]);
