@@ -529,11 +529,16 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     a.chunk_vecs = p.chunk_vecs;
     a.nbuf = (uint32_t)p.nbuf;
     // single-buffered slices (the backward of large channels): the refill waits for the
-    // apply, so the slice is prefetched into L2 first (cfg4 backward 0.90 -> 0.85 ms;
-    // double-buffered kernels measured slightly slower with it)
+    // apply, so the slice is prefetched into L2 first (cfg4 backward 0.90 -> 0.85 ms).
+    // Double-buffered slices of large planes (>= 16 KB: one prefetch per plane) too: the
+    // fused-collective sync over 2-8 ranks on cfg4 (one plane per CTA) 77-79 -> 82-85 %
+    // of peak; small planes (r50s3, 14x14 bf16) measured slower with it (tools/gpu_exp122.sh)
     {
         const int pf = env_int("IABN_FUSED_PREFETCH", -1);  // -1 auto, 0 off, 1 on, 2 bwd only
-        a.prefetch = pf < 0 ? (p.nbuf == 1 ? 1u : 0u) : pf == 2 ? (uint32_t)(pass == 1) : (uint32_t)pf;
+        const bool big_planes = a.HW * (int64_t)sizeof(T) >= 16384;
+        a.prefetch = pf < 0    ? (p.nbuf == 1 || big_planes ? 1u : 0u)
+                     : pf == 2 ? (uint32_t)(pass == 1)
+                               : (uint32_t)pf;
         // L2 cache hints: bit 1 = the prefetch marks its lines evict_last (they must survive
         // until the refill), bit 2 = the refill copies mark them evict_first (used once);
         // measured: backward 0.848 -> 0.834 ms, DRAM reads 3.45 -> 3.32 GB (3.29 GB minimum)
