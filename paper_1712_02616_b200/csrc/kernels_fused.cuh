@@ -354,9 +354,18 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
 
     if (warp == kProducerWarp) {
         // ================================================ producer: slab t into buffer t % nbuf,
-        // chunk by chunk: chunk k is refilled as soon as the apply warps released it
-        if (lane == 0) {
+        // chunk by chunk: chunk k is refilled as soon as the apply warps released it.  The
+        // bulk copies of a chunk (one per plane) are spread over the warp's lanes: small
+        // layers have 16-64 planes per slice, issued serially they delay the first arrival
+        // (r50s3 backward 35.1 -> 34.0 us).  Chunks of 1-3 planes stay on lane 0 (cfg4
+        // backward 0.835 -> 0.839 ms with the whole warp in the loop).
+        const uint64_t chunk_bytes = (uint64_t)a.chunk_vecs * 16u;
+        const bool wide = !(a.debug & 8u) &&  // experiments: lane 0 issues all
+                          (MIS ? a.chunk_vecs >= 4u * a.mis_w
+                               : chunk_bytes >= 4u * (uint64_t)a.HW * sizeof(T));
+        if (wide || lane == 0) {
             constexpr bool kL2Hints = MINB == 2;
+            const uint32_t nl = wide ? 32u : 1u;  // lanes issuing copies
             const T* src[2] = {(const T*)a.in0 + voff, (const T*)a.in1 + voff};
             const uint32_t hw = (uint32_t)a.HW;
             for (uint32_t t = 0; t < nT; ++t) {
@@ -369,7 +378,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 // them: compiled out of the 4-CTA/SM one, measured ~3 % slower on r50s3 with)
                 const bool hint_first =
                     kL2Hints && (((a.prefetch & 4u) && t >= nbuf) || (a.prefetch & 8u));
-                if ((a.prefetch & 1u) && t >= nbuf) {
+                if (lane == 0 && (a.prefetch & 1u) && t >= nbuf) {
                     // the slice's buffer is still being applied: pull the slice into L2 now,
                     // so that the bulk copies issued as its chunks free up hit L2 (HBM
                     // latency off the refill path; bytes read from HBM once either way)
@@ -411,18 +420,20 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     }
                     const uint32_t c_lo = vlo + k * a.chunk_vecs;
                     const uint32_t c_hi = min(vhi, c_lo + a.chunk_vecs);
-                    if (k == 0) IABN_TRACE(a, t, 0);
-                    if (k == nch - 1) IABN_TRACE(a, t, 1);
+                    if (lane == 0 && k == 0) IABN_TRACE(a, t, 0);
+                    if (lane == 0 && k == nch - 1) IABN_TRACE(a, t, 1);
                     if constexpr (MIS) {
                         // planes [n_lo, n_hi) of the chunk: copy each one's covering range
                         const uint32_t n_lo = c_lo / a.mis_w, n_hi = c_hi / a.mis_w;
                         uint32_t bytes = 0;
-                        for (uint32_t n = n_lo; n < n_hi; ++n) {
+                        for (uint32_t n = n_lo + lane; lane < nl && n < n_hi; n += nl) {
                             const MisPlane mp = mis_plane((uint64_t)n * a.C + c, a.hwb);
                             bytes += (uint32_t)(((mp.a0 + mp.h + a.hwb + 15) & ~(uint64_t)15) - mp.a0);
                         }
-                        mbar_arrive_expect_tx(&full[b][k], bytes * NIN);
-                        for (uint32_t n = n_lo; n < n_hi; ++n) {
+                        if (wide) bytes = __reduce_add_sync(0xffffffffu, bytes);
+                        if (lane == 0) mbar_arrive_expect_tx(&full[b][k], bytes * NIN);
+                        if (wide) __syncwarp();
+                        for (uint32_t n = n_lo + lane; lane < nl && n < n_hi; n += nl) {
                             const MisPlane mp = mis_plane((uint64_t)n * a.C + c, a.hwb);
                             const uint32_t nb =
                                 (uint32_t)(((mp.a0 + mp.h + a.hwb + 15) & ~(uint64_t)15) - mp.a0);
@@ -433,14 +444,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         }
                         continue;
                     }
-                    mbar_arrive_expect_tx(&full[b][k], (c_hi - c_lo) * 16u * NIN);
-                    uint32_t j = c_lo * V;  // channel-space element
-                    const uint32_t jend = c_hi * V;
-                    uint32_t n = fdiv(j, a.fd_hw);
-                    uint32_t sp = j - n * hw;
-                    while (j < jend) {
-                        const uint32_t len = min(jend - j, hw - sp);
-                        const int64_t goff = ((int64_t)n * a.C + c) * a.HW + sp;
+                    if (lane == 0) mbar_arrive_expect_tx(&full[b][k], (c_hi - c_lo) * 16u * NIN);
+                    if (wide) __syncwarp();
+                    // one bulk copy per plane piece of the chunk
+                    auto copy = [&](uint32_t j, uint32_t len, int64_t goff) {
 #pragma unroll
                         for (int i = 0; i < NIN; ++i) {
                             if (hint_first)
@@ -451,9 +458,28 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                                 bulk_g2s(buf + (size_t)i * a.cap + (j / V - vlo), src[i] + goff,
                                          len * (uint32_t)sizeof(T), &full[b][k]);
                         }
-                        j += len;
-                        ++n;
-                        sp = 0;
+                    };
+                    const uint32_t j0 = c_lo * V, jend = c_hi * V;  // channel-space elements
+                    if (wide) {
+                        // plane n holds [n * hw, (n + 1) * hw); lane l takes planes l, l + 32, ..
+                        for (uint32_t n = fdiv(j0, a.fd_hw) + lane;; n += 32) {
+                            const uint64_t ps = (uint64_t)n * hw;
+                            if (ps >= jend) break;
+                            const uint32_t j = ps > j0 ? (uint32_t)ps : j0;
+                            const uint32_t len = (ps + hw < jend ? (uint32_t)(ps + hw) : jend) - j;
+                            copy(j, len, ((int64_t)n * a.C + c) * a.HW + (j - (uint32_t)ps));
+                        }
+                    } else {
+                        uint32_t j = j0;
+                        uint32_t n = fdiv(j, a.fd_hw);
+                        uint32_t sp = j - n * hw;
+                        while (j < jend) {
+                            const uint32_t len = min(jend - j, hw - sp);
+                            copy(j, len, ((int64_t)n * a.C + c) * a.HW + sp);
+                            j += len;
+                            ++n;
+                            sp = 0;
+                        }
                     }
                 }
             }
