@@ -1,7 +1,7 @@
 """ctypes binding of libiabn.so (include/iabn.h).  Argument marshalling only.
 
 The shared library is loaded from this package directory (built in-tree by
-``paper_1712_02616_b200.build``).  There is no fallback: if the library is
+``paper_1712_02616_b200/build.py``).  There is no fallback: if the library is
 missing, importing this module raises.
 """
 from __future__ import annotations
@@ -60,7 +60,7 @@ _DP = ctypes.POINTER(Desc)
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1712_02616_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_1712_02616_b200/build.py` "
             "(there is no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     lib.iabn_version.restype = ctypes.c_int

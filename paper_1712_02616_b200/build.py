@@ -1,6 +1,6 @@
 """Build libiabn.so in-tree with nvcc for sm_100a (B200).
 
-    python -m paper_1712_02616_b200.build [--force] [--verbose]
+    python paper_1712_02616_b200/build.py [--force] [--verbose]
 
 The library links the CUDA runtime statically (it coexists with torch's own
 cudart) and loads NCCL at run time with dlopen, so it loads on a machine

@@ -198,3 +198,19 @@ def test_sync_emulated_validation():
                                            1e-5, 0.01, 0, P * 16,
                                            L.workspace_bytes(L.desc(4, 8, 16, L.F32, L.NCHW)), None)
     assert st == L.ERR_INVALID_ARG  # save_var NULL
+
+
+def test_build_entry_does_not_import_package_before_library_exists():
+    """build() must work from a fresh checkout (libiabn.so is git-ignored): the build
+    script is loaded by path, so the package (which raises without the library) is not
+    imported before the library is built."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import importlib.util, sys, os;"
+            "spec = importlib.util.spec_from_file_location('_b', "
+            "os.path.join(sys.argv[1], 'paper_1712_02616_b200', 'build.py'));"
+            "m = importlib.util.module_from_spec(spec); spec.loader.exec_module(m);"
+            "assert 'paper_1712_02616_b200' not in sys.modules;"
+            "assert callable(m.build) and m.LIB.endswith('libiabn.so')")
+    subprocess.run([sys.executable, "-c", code, root], check=True, cwd="/")
