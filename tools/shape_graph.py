@@ -13,6 +13,9 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1712_02616_b200 as P  # noqa: E402
 
+PEAK_GBS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                       "MEASURED_PEAKS.json")))["hbm_gbs"]
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--layout", default="NHWC")
 ap.add_argument("--dtype", default="bf16")
@@ -54,5 +57,5 @@ for sh in args.shapes.split(","):
     e1.record()
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / (5 * R) * 1e3
-    res[sh] = dict(us_per_layer=round(us, 2), pct_of_peak=round(100 * 5 * nbytes / (us * 1e-6) / 6536e9, 1))
+    res[sh] = dict(us_per_layer=round(us, 2), pct_of_peak=round(100 * 5 * nbytes / (us * 1e-6) / (PEAK_GBS * 1e9), 1))
 print(json.dumps(dict(layout=args.layout, dtype=args.dtype, N=args.N, **res)))
