@@ -12,7 +12,8 @@ conv_b, with conv_a a 1x1 conv producing the stage width W and conv_b the groupe
 3x3 conv (32 groups) of a ResNeXt-101 32x4d bottleneck; stages W = 128, 256, 512,
 1024 at 56^2, 28^2, 14^2, 7^2 (Conv1-Conv4).  The convolutions are cuDNN (library
 code, identical in all three); only the BN+Act differs.  Reported: mean fwd+bwd
-time (CUDA events), its increase over `standard`, and the peak memory of one
+time (CUDA events; eager, and the same step replayed from a CUDA graph), its
+increase over `standard`, and the peak memory of one
 forward+backward above the resident parameters and input.
 
     python tools/fig4_blocks.py [--dtype f32|bf16] [--iters 200]
@@ -82,7 +83,32 @@ def measure(width, hw, strategy, dtype, iters, device):
         step()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters, peak
+    eager_ms = e0.elapsed_time(e1) / iters
+    # the same step captured in a CUDA graph: device time without the host-side launch
+    # cost (at 14^2 and 7^2 the eager steps are bound by it in every variant)
+    graph_ms, graph_err = None, None
+    try:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                step()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        for _ in range(5):
+            g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(iters):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        graph_ms = e0.elapsed_time(e1) / iters
+    except Exception as e:  # reported, not hidden
+        graph_err = f"{type(e).__name__}: {e}"[:200]
+    return eager_ms, peak, graph_ms, graph_err
 
 
 def main():
@@ -97,11 +123,17 @@ def main():
     for name, width, hw in STAGES:
         res = {}
         for strategy in ("standard", "inplace_abn", "checkpointing"):
-            ms, peak = measure(width, hw, strategy, dtype, args.iters, dev)
-            res[strategy] = dict(ms=round(ms, 4), peak_mb=round(peak / 2**20, 1))
+            ms, peak, gms, gerr = measure(width, hw, strategy, dtype, args.iters, dev)
+            res[strategy] = dict(ms=round(ms, 4), peak_mb=round(peak / 2**20, 1),
+                                 graph_ms=None if gms is None else round(gms, 4))
+            if gerr:
+                res[strategy]["graph_error"] = gerr
         std = res["standard"]
         for s in ("inplace_abn", "checkpointing"):
             res[s]["time_vs_standard_pct"] = round(100 * (res[s]["ms"] / std["ms"] - 1), 1)
+            if res[s]["graph_ms"] is not None and std["graph_ms"] is not None:
+                res[s]["graph_time_vs_standard_pct"] = round(
+                    100 * (res[s]["graph_ms"] / std["graph_ms"] - 1), 1)
             res[s]["memory_vs_standard_pct"] = round(100 * (res[s]["peak_mb"] / std["peak_mb"] - 1), 1)
         rows.append(dict(block=name, width=width, hw=hw, batch=32, **res))
     print(json.dumps(dict(dtype=args.dtype, iters=args.iters, blocks=rows), indent=1))
