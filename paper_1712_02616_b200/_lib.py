@@ -109,8 +109,16 @@ def check(status: int, fn: str) -> None:
         raise IabnError(status, fn, lib.iabn_last_error().decode())
 
 
+_FNS: dict = {}
+
+
 def call(name: str, *args) -> None:
-    check(getattr(lib, name)(*args), name)
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(lib, name)
+    st = fn(*args)
+    if st != OK:
+        check(st, name)
 
 
 def launch_count() -> int:

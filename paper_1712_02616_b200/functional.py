@@ -48,19 +48,35 @@ def _geom(x: torch.Tensor, layout: str) -> tuple[int, int, int]:
     return n, c, hw
 
 
+_DESCS: dict[tuple, L.Desc] = {}
+
+
 def _desc(x: torch.Tensor, layout: str) -> L.Desc:
+    """Descriptor of x, cached per (shape, dtype, layout): a layer calls with the same
+    shape every step, and building the ctypes struct is part of the per-call host cost."""
+    key = (x.shape, x.dtype, layout, x.is_cuda)
+    d = _DESCS.get(key)
+    if d is not None and x.is_contiguous():
+        return d
     n, c, hw = _geom(x, layout)
-    return L.desc(n, c, hw, _DTYPES[x.dtype], _LAYOUT[layout])
+    d = L.desc(n, c, hw, _DTYPES[x.dtype], _LAYOUT[layout])
+    if len(_DESCS) < 4096:
+        _DESCS[key] = d
+    return d
 
 
 _WS: dict[tuple, torch.Tensor] = {}
+_WSB: dict[tuple, int] = {}  # workspace bytes per geometry (pure function of the desc)
 
 
 def workspace(d: L.Desc, device: torch.device, stream=None) -> tuple[int, int]:
     """Scratch space of the call: one buffer per (device, stream), grown on demand.
     Calls on one stream are ordered, so they may share it; calls on different
     streams get different buffers (the library's calls are stream-ordered only)."""
-    nbytes = max(L.workspace_bytes(d), 16)
+    dk = (d.n, d.c, d.hw, d.dtype, d.layout)
+    nbytes = _WSB.get(dk)
+    if nbytes is None:
+        nbytes = _WSB[dk] = max(L.workspace_bytes(d), 16)
     key = (device.index, _stream(stream))
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
@@ -81,9 +97,16 @@ def _f32(t: torch.Tensor | None, C: int, name: str) -> torch.Tensor | None:
     return t
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_CUR_DEV = getattr(torch._C, "_cuda_getDevice", None)
+
+
 def _stream(stream) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    if _RAW_STREAM is not None and _CUR_DEV is not None:  # same value, without the Stream object
+        return _RAW_STREAM(_CUR_DEV())
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _flags(gamma_mode: str, running_var_biased: bool = False, extra: int = 0) -> int:

@@ -78,4 +78,41 @@ for _ in range(500):
 e1.record()
 torch.cuda.synchronize()
 res["graph_device_us_per_pair"] = round(e0.elapsed_time(e1) / 500 * 1e3, 2)
+# Host cost per call without back-pressure: the loops above enqueue thousands of
+# launches, so the launch queue fills and the host time tracks the device time.  Here
+# short bursts (the queue never fills; the GPU is idle at the start of each burst),
+# per entry point, with the kernels each call launches.
+def raw_fwd():
+    L.lib.iabn_forward(*fa)
+
+
+def raw_bwd():
+    L.lib.iabn_backward(*ba)
+
+
+def py_fwd():
+    P.forward(x, g, b, rm, rv)
+
+
+def py_bwd():
+    P.backward(x, dz, g, b, sv)
+
+
+burst = {}
+for name, fn in (("raw_forward", raw_fwd), ("raw_backward", raw_bwd), ("python_forward", py_fwd),
+                 ("python_backward", py_bwd)):
+    ts = []
+    for _ in range(40):
+        torch.cuda.synchronize()
+        k0 = L.launch_count()
+        t0 = time.perf_counter()
+        for _ in range(8):
+            fn()
+        ts.append((time.perf_counter() - t0) / 8 * 1e6)
+        k = (L.launch_count() - k0) / 8
+    ts.sort()
+    burst[name] = dict(host_us_per_call_median=round(ts[len(ts) // 2], 2),
+                       host_us_per_call_min=round(ts[0], 2), kernels_per_call=k)
+torch.cuda.synchronize()
+res["burst_of_8_calls"] = burst
 print(json.dumps(dict(shape=[N, C, HW], **res)))
