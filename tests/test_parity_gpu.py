@@ -498,3 +498,25 @@ def test_sync_through_nccl_single_rank(case):
         compare(case, got, run_oracle(case, x, dz, p), p)
     finally:
         comm.close()
+
+
+def test_binding_desc_cache_keeps_validation():
+    """The binding caches descriptors per (shape, dtype, layout): a cached shape must
+    still reject a non-contiguous tensor, and two shapes must not share a descriptor."""
+    import paper_1712_02616_b200 as P
+    dev = torch.device("cuda", 0)
+    C = 16
+    g, b = torch.ones(C, device=dev), torch.zeros(C, device=dev)
+    x = torch.randn(4, C, 8, 8, device=dev)
+    z1, m1, v1 = P.forward(x.clone(), g, b)
+    xt = torch.randn(4, 8, 8, C, device=dev).permute(0, 3, 1, 2)  # same shape, strided
+    assert xt.shape == x.shape and not xt.is_contiguous()
+    with pytest.raises(ValueError):
+        P.forward(xt, g, b)
+    y = torch.randn(2, C, 8, 8, device=dev)
+    z2, m2, v2 = P.forward(y.clone(), g, b)
+    torch.cuda.synchronize()
+    ref = y.double().transpose(0, 1).reshape(C, -1)
+    assert torch.allclose(m2.double().cpu(), ref.mean(1).cpu(), atol=1e-5)
+    assert torch.allclose(m1.double().cpu(), x.double().transpose(0, 1).reshape(C, -1).mean(1).cpu(),
+                          atol=1e-5)
