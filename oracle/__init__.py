@@ -62,6 +62,9 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
               lib.oracle_backward_standard, lib.oracle_backward_inplace_I,
               lib.oracle_backward_inplace_II, lib.oracle_merge_stats, lib.oracle_fold_conv):
         f.restype = None
+    lib.oracle_param_grads_sharded.argtypes = [_I64, _I64, _I64, i, _D, _D, _D, _D, i, d, d, _I64,
+                                               ctypes.POINTER(_I64), _D, _D]
+    lib.oracle_param_grads_sharded.restype = None
     lib.oracle_mutant_id.restype = ctypes.c_int
     return lib
 
@@ -182,6 +185,22 @@ class Oracle:
                             gamma_mode="abs_eps", layout="NCHW"):
         return self._bwd_from_z(self.lib.oracle_backward_inplace_II, z, dz, var, gamma, beta, eps,
                                 slope, gamma_mode, layout)
+
+    def param_grads_sharded(self, x, dz, gamma, beta, shards, *, eps=1e-5, slope=0.01,
+                            gamma_mode="abs_eps", layout="NCHW"):
+        """Per-shard (dgamma, dbeta), each [len(shards), C], of the synchronized layer over
+        the concatenated batch x (shard k = the next shards[k] samples along N; R7)."""
+        x, dz = _f64(x), _f64(dz)
+        N, C, HW = _shape(x, layout)
+        assert sum(shards) == N
+        K = len(shards)
+        sn = (_I64 * K)(*[int(s) for s in shards])
+        dg, db = np.empty((K, C)), np.empty((K, C))
+        self.lib.oracle_param_grads_sharded(N, C, HW, LAYOUTS[layout], _p(x), _p(dz),
+                                            _p(_f64(gamma)), _p(_f64(beta)),
+                                            GAMMA_MODES[gamma_mode], eps, slope, K, sn, _p(dg),
+                                            _p(db))
+        return dg, db
 
     def merge_stats(self, counts, means, vars_):
         counts, means, vars_ = _f64(counts), _f64(means), _f64(vars_)

@@ -19,8 +19,9 @@
  * Pins: tests/test_oracle_pins.py (worked examples, closed forms, finite
  * differences, PyTorch float64, three-way equivalence, mutation tests).
  * Parity unpinned (pinned only to our reading): running-var estimator and
- * momentum convention (R3), the |gamma|+eps reparametrisation (R4), the
- * subgradient at 0 (R5), local dgamma/dbeta under sync (R7).
+ * momentum convention (R3; the biased branch is pinned to SPEC.md's reading), the
+ * |gamma|+eps reparametrisation (R4), the subgradient at 0 (R5), local dgamma/dbeta
+ * under sync (R7; pinned by their sum, the whole-batch gradient).
  */
 #include <math.h>
 #include <stddef.h>
@@ -173,6 +174,9 @@ void oracle_forward(int64_t N, int64_t C, int64_t HW, int layout, const double *
         if (running_var) {
 #if ORACLE_MUTANT == 10
             const double v = var; /* mutant: Bessel correction dropped */
+            (void)running_var_biased;
+#elif ORACLE_MUTANT == 13
+            const double v = var * m / (m - 1.0); /* mutant: running_var_biased ignored */
             (void)running_var_biased;
 #else
             const double v = running_var_biased ? var : var * m / (m - 1.0);
@@ -406,6 +410,55 @@ void oracle_fold_conv(int64_t cout, int64_t kper, const double *w, const double 
 #else
         bias_out[k] = s * (b - running_mean[k]) + beta[k];
 #endif
+    }
+}
+
+/*
+ * Parameter gradients of each shard under InPlace-ABN^sync (PAPER.md:315 statistics
+ * of the whole, "virtual" batch; :356 "gradient-synchronized"), reading R7: every rank
+ * returns its own contribution to dL/dbeta and dL/dgamma, so that the caller's
+ * data-parallel gradient sum yields the gradient of the whole batch.  With x the
+ * concatenation of the shards along N (shard k = samples [o_k, o_k + shard_n[k])),
+ * mu and sigma^2 are those of the whole batch and, per shard k,
+ *   dbeta_k   = sum_{i in k} dy_i
+ *   dgamma~_k = sum_{i in k} dy_i x^_i
+ * with x^_i, y_i from stored x (Eq.(1)) and dy_i = f'(y_i) dz_i; dgamma_k =
+ * dgamma~_k d gamma~/d gamma (R4).  Outputs are [nshards][C].
+ */
+void oracle_param_grads_sharded(int64_t N, int64_t C, int64_t HW, int layout, const double *x,
+                                const double *dz, const double *gamma, const double *beta,
+                                int gamma_mode, double eps, double slope, int64_t nshards,
+                                const int64_t *shard_n, double *dgamma, double *dbeta)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < C; ++c) {
+        double mu, var;
+        channel_stats(N, C, HW, layout, x, c, &mu, &var);
+        const double rstd = 1.0 / sqrt(var + eps);
+        const double g = gamma_eff(gamma_mode, gamma[c], eps);
+        int64_t n0 = 0;
+        for (int64_t k = 0; k < nshards; ++k) {
+#if ORACLE_MUTANT == 12
+            /* mutant: the shard's own statistics instead of the whole batch's */
+            channel_stats(shard_n[k], C, HW, layout, x + (size_t)n0 * C * HW, c, &mu, &var);
+            const double rstd_k = 1.0 / sqrt(var + eps);
+#else
+            const double rstd_k = rstd;
+#endif
+            double sdy = 0.0, sdyxh = 0.0;
+            for (int64_t n = n0; n < n0 + shard_n[k]; ++n)
+                for (int64_t s = 0; s < HW; ++s) {
+                    const size_t i = at(layout, C, HW, n, c, s);
+                    const double xhat = (x[i] - mu) * rstd_k;
+                    const double y = g * xhat + beta[c];
+                    const double dy = leaky_deriv(y, slope) * dz[i];
+                    sdy += dy;
+                    sdyxh += dy * xhat;
+                }
+            dbeta[k * C + c] = sdy;
+            dgamma[k * C + c] = sdyxh * gamma_eff_deriv(gamma_mode, gamma[c]);
+            n0 += shard_n[k];
+        }
     }
 }
 

@@ -43,5 +43,9 @@ void oracle_fold_conv(int64_t cout, int64_t kper, const double *w, const double 
                       const double *running_mean, const double *running_var,
                       const double *gamma, const double *beta, int gamma_mode, double eps,
                       double *w_out, double *bias_out);
+void oracle_param_grads_sharded(int64_t N, int64_t C, int64_t HW, int layout, const double *x,
+                                const double *dz, const double *gamma, const double *beta,
+                                int gamma_mode, double eps, double slope, int64_t nshards,
+                                const int64_t *shard_n, double *dgamma, double *dbeta);
 int oracle_mutant_id(void);
 #endif

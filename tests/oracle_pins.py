@@ -94,6 +94,17 @@ def pin_golden_running(o):
     assert abs(r.running_mean[0] - g["expected"]) < 1e-12
 
 
+def pin_golden_running_biased(o):
+    """IABN_RUNNING_VAR_BIASED follows SPEC.md's reading (:224, :272): the running
+    variance is updated with the biased batch variance."""
+    g = _golden()["running_update_var_biased"]
+    x = np.array(g["x"]).reshape(-1, 1, 1)
+    r = o.forward(x, [1.0], [0.0], momentum=g["momentum"], running_mean=[g["running_mean"]],
+                  running_var=[g["running_var"]], running_var_biased=True)
+    assert abs(r.running_mean[0] - g["expected_running_mean"]) < 1e-12
+    assert abs(r.running_var[0] - g["expected_running_var"]) < 1e-12
+
+
 def pin_golden_sync(o):
     g = _golden()["sync_merge"]
     shards = [np.array(s).reshape(-1, 1, 1) for s in g["shards"]]
@@ -302,6 +313,28 @@ def pin_sync_concat(o):
         assert np.max(np.abs(mm - mean)) < 1e-12 and np.max(np.abs(vv - var)) < 1e-12
 
 
+def pin_sharded_param_grads(o):
+    """Per-shard dgamma/dbeta of the synchronized layer (R7): their sum
+    over shards is the whole batch's gradient (the brute-force/torch-pinned
+    backward_standard); one shard is the whole batch; a batch made of two copies of x
+    gives each copy x's own gradient (the statistics of [x; x] are those of x)."""
+    for layout in ("NCHW", "NHWC"):
+        for mode in ("abs_eps", "plain"):
+            x, dz, gamma, beta = _rand_problem(7, 5, 6, seed=21, layout=layout)
+            _, dg, db = o.backward_standard(x, dz, gamma, beta, gamma_mode=mode, layout=layout)
+            sdg, sdb = o.param_grads_sharded(x, dz, gamma, beta, [2, 3, 2], gamma_mode=mode,
+                                             layout=layout)
+            assert vec_err(sdg.sum(0), dg) < 1e-12 and vec_err(sdb.sum(0), db) < 1e-12
+            one_g, one_b = o.param_grads_sharded(x, dz, gamma, beta, [7], gamma_mode=mode,
+                                                 layout=layout)
+            assert vec_err(one_g[0], dg) < 1e-13 and vec_err(one_b[0], db) < 1e-13
+            x2, dz2 = np.concatenate([x, x]), np.concatenate([dz, dz])
+            hg, hb = o.param_grads_sharded(x2, dz2, gamma, beta, [7, 7], gamma_mode=mode,
+                                           layout=layout)
+            for k in range(2):
+                assert vec_err(hg[k], dg) < 1e-12 and vec_err(hb[k], db) < 1e-12
+
+
 def pin_permute_batch(o):
     x, dz, gamma, beta = _rand_problem(5, 4, 6, seed=12)
     perm = np.array([3, 0, 4, 1, 2])
@@ -347,7 +380,8 @@ def pin_fold_conv(o):
         assert (folded - two_stage).abs().max().item() < 1e-12 * max(1.0, two_stage.abs().max().item())
 
 
-PINS = [pin_golden_bn, pin_golden_leaky, pin_golden_running, pin_golden_sync, pin_whitening,
+PINS = [pin_golden_bn, pin_golden_leaky, pin_golden_running, pin_golden_running_biased,
+        pin_golden_sync, pin_sharded_param_grads, pin_whitening,
         pin_const_dz, pin_dx_moments, pin_torch_f64, pin_torch_eval, pin_finite_diff,
         pin_three_way, pin_fixed_one, pin_scaling, pin_sync_concat, pin_permute_batch,
         pin_golden_fold, pin_fold_conv]
