@@ -170,6 +170,7 @@ IABN_API iabn_status iabn_backward(const iabn_desc *desc, const void *z, const v
  * per-channel (count, sum, sum of squares) are summed over ranks in fp64 with
  * ncclAllReduce on `stream` between the reduction and the apply kernels; the
  * backward sums (sum dy, sum dy x^) likewise.  Shards may have different n.
+ * nranks == 1 takes the non-synchronized path (no collective).
  * NCCL is loaded at run time (libnccl.so.2); without it these return
  * IABN_ERR_NCCL.  id: 128 opaque bytes from rank 0, distributed by the caller. */
 IABN_API iabn_status iabn_comm_get_unique_id(unsigned char id[128]);
@@ -186,6 +187,19 @@ IABN_API iabn_status iabn_backward_sync(const iabn_desc *desc, const void *z, co
                                const float *save_var, float *dgamma, float *dbeta, float eps,
                                float slope, uint32_t flags, void *ws, size_t ws_bytes,
                                void *stream, iabn_comm comm);
+
+/* Per-phase device time of the synchronized calls (measurement; SURVEY.md section 8(d)
+ * item 3).  With timing on, iabn_forward_sync / iabn_backward_sync record CUDA events
+ * on their stream around [local reduction | all-reduce | apply] (the all-reduce is the
+ * library's own ncclAllReduce call); iabn_comm_phase_ms waits for the last recorded
+ * events and writes ms[6] = forward {reduce, all-reduce, apply}, backward {reduce,
+ * all-reduce, apply} of the most recent calls (-1 where a pass has not run since timing
+ * was switched on).  The fused-collective kernels exchange inside the kernel: their
+ * whole pass is reported as "reduce", all-reduce and apply as 0.  Off by default (the
+ * events cost ~1 us per phase and break the PDL overlap between the phases).
+ * Errors: IABN_ERR_INVALID_ARG (NULL comm / ms), IABN_ERR_CUDA. */
+IABN_API iabn_status iabn_comm_set_timing(iabn_comm comm, int on);
+IABN_API iabn_status iabn_comm_phase_ms(iabn_comm comm, float ms[6]);
 
 /* ------------------------------------------------------------------ fused-collective sync
  * With IABN_SYNC_FUSED (NCHW shapes the channel-resident schedule takes, at most 8

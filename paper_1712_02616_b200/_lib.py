@@ -36,7 +36,8 @@ EXPORTS = ["iabn_version", "iabn_status_string", "iabn_last_error", "iabn_launch
            "iabn_comm_get_unique_id", "iabn_comm_init", "iabn_comm_destroy", "iabn_forward_sync",
            "iabn_backward_sync", "iabn_forward_reduce", "iabn_forward_apply",
            "iabn_backward_reduce", "iabn_backward_apply", "iabn_fold_conv",
-           "iabn_forward_sync_emulated", "iabn_backward_sync_emulated"]
+           "iabn_forward_sync_emulated", "iabn_backward_sync_emulated", "iabn_comm_set_timing",
+           "iabn_comm_phase_ms"]
 
 
 class Desc(ctypes.Structure):
@@ -78,6 +79,8 @@ def _load() -> ctypes.CDLL:
     lib.iabn_comm_get_unique_id.argtypes = [ctypes.c_char_p]
     lib.iabn_comm_init.argtypes = [ctypes.POINTER(_P), ctypes.c_int, ctypes.c_int, ctypes.c_char_p]
     lib.iabn_comm_destroy.argtypes = [_P]
+    lib.iabn_comm_set_timing.argtypes = [_P, ctypes.c_int]
+    lib.iabn_comm_phase_ms.argtypes = [_P, ctypes.POINTER(ctypes.c_float)]
     lib.iabn_forward_sync.argtypes = lib.iabn_forward.argtypes + [_P]
     lib.iabn_backward_sync.argtypes = lib.iabn_backward.argtypes + [_P]
     lib.iabn_forward_reduce.argtypes = [_DP, _P, _P, _P, _SZ, _P]

@@ -967,6 +967,16 @@ struct SyncBuf {
 
 }  // namespace
 
+// What the ranks agreed on for one (shard geometry, pass) of the fused-collective sync:
+// whether every rank can run the channel-resident kernel with the same plan (same
+// channel -> cluster mapping, equal shards), and the global count m_G.
+struct SyncAgree {
+    int64_t n, c, hw;
+    int dtype, layout, pass;
+    bool fused;
+    int64_t m_global;
+};
+
 struct iabn_comm_s {
     ncclComm_t comm;
     int nranks, rank;
@@ -974,6 +984,11 @@ struct iabn_comm_s {
     // buffer mapped through CUDA IPC (peer access over NVLink), the call counter
     SyncBuf sb{};
     void* own = nullptr;
+    std::vector<SyncAgree> agree{};
+    // phase timing (iabn_comm_set_timing): events [pass][4] around reduce | all-reduce | apply
+    bool timing = false;
+    bool timed[2] = {false, false};
+    cudaEvent_t ev[2][4] = {};
 };
 
 namespace {
@@ -1005,18 +1020,21 @@ iabn_status comm_sync_buf(iabn_comm comm, int64_t C, cudaStream_t st) {
     const size_t bytes = (size_t)2 * cap * comm->nranks * sizeof(PeerRec);
     void* nb = nullptr;
     IABN_TRY(cuda(cudaMalloc(&nb, bytes), "cudaMalloc"));
-    IABN_TRY(cuda(cudaMemset(nb, 0, bytes), "cudaMemset"));
+    // stream-ordered initialisation (the caller's stream may be a non-blocking one, which
+    // the legacy-stream cudaMemset / cudaMemcpy would not be ordered with)
+    IABN_TRY(cuda(cudaMemsetAsync(nb, 0, bytes, st), "cudaMemsetAsync"));
     if (!comm->sb.ctr) {
-        const unsigned long long init[2] = {1ull, 0ull};
+        static const unsigned long long init[2] = {1ull, 0ull};
         IABN_TRY(cuda(cudaMalloc(&comm->sb.ctr, sizeof(init)), "cudaMalloc"));
-        IABN_TRY(cuda(cudaMemcpy(comm->sb.ctr, init, sizeof(init), cudaMemcpyHostToDevice), "counter"));
+        IABN_TRY(cuda(cudaMemcpyAsync(comm->sb.ctr, init, sizeof(init), cudaMemcpyHostToDevice, st),
+                      "counter"));
     }
     cudaIpcMemHandle_t h;
     IABN_TRY(cuda(cudaIpcGetMemHandle(&h, nb), "cudaIpcGetMemHandle"));
     const size_t hb = sizeof(cudaIpcMemHandle_t);
     char* dh = nullptr;
     IABN_TRY(cuda(cudaMalloc(&dh, hb * comm->nranks), "cudaMalloc"));
-    IABN_TRY(cuda(cudaMemcpy(dh + hb * comm->rank, &h, hb, cudaMemcpyHostToDevice), "handle"));
+    IABN_TRY(cuda(cudaMemcpyAsync(dh + hb * comm->rank, &h, hb, cudaMemcpyHostToDevice, st), "handle"));
     const ncclResult_t r = n->AllGather(dh + hb * comm->rank, dh, hb, ncclInt8, comm->comm, st);
     if (r != ncclSuccess) return fail(IABN_ERR_NCCL, "ncclAllGather: %s", n->GetErrorString(r));
     std::vector<cudaIpcMemHandle_t> hs(comm->nranks);
@@ -1039,8 +1057,70 @@ iabn_status comm_sync_buf(iabn_comm comm, int64_t C, cudaStream_t st) {
     return IABN_OK;
 }
 
+// Phase boundary k (0..3) of pass `pass` of a timed synchronized call.
+void phase_mark(iabn_comm comm, int pass, int k, cudaStream_t st) {
+    if (!comm->timing) return;
+    if (!comm->ev[pass][k] && cudaEventCreate(&comm->ev[pass][k]) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    cudaEventRecord(comm->ev[pass][k], st);
+    if (k == 3) comm->timed[pass] = true;
+}
+
 bool sync_fused_wanted(uint32_t flags) {
     return (flags & IABN_SYNC_FUSED) || env_int("IABN_SYNC_FUSED", 0) == 1;
+}
+
+// Collective (every rank, same call): do all ranks run the fused-collective kernel for
+// this shard geometry and pass?  The kernels of different ranks wait on one another per
+// channel, so they must agree -- same shard shape and same plan (K, clusters, nbuf: the
+// channel -> cluster order) on every rank -- or all take the reduce / all-reduce / apply
+// path.  Decided once per (geometry, pass) by an all-gather of each rank's plan (a host
+// synchronisation: the first call of a shape must not be inside a CUDA-graph capture),
+// then cached in the communicator.
+iabn_status sync_agree(iabn_comm comm, const Geom& g, int pass, const FusedPlan& p,
+                       cudaStream_t st, SyncAgree* out) {
+    for (const SyncAgree& a : comm->agree)
+        if (a.n == g.N && a.c == g.C && a.hw == g.HW && a.dtype == g.dtype &&
+            a.layout == g.layout && a.pass == pass) {
+            *out = a;
+            return IABN_OK;
+        }
+    Nccl* n = nccl();
+    if (!n || !n->AllGather) return fail(IABN_ERR_NCCL, "NCCL all-gather unavailable");
+    constexpr int R = 8;
+    const int64_t mine[R] = {g.N, g.C, g.HW, (int64_t)g.dtype | ((int64_t)g.layout << 8),
+                             p.ok ? 1 : 0, p.K, p.clusters, p.nbuf};
+    int64_t* d = nullptr;
+    auto cuda = [](cudaError_t e, const char* what) -> iabn_status {
+        return e == cudaSuccess ? IABN_OK
+                                : fail(IABN_ERR_CUDA, "sync schedule agreement, %s: %s", what,
+                                       cudaGetErrorString(e));
+    };
+    IABN_TRY(cuda(cudaMalloc(&d, sizeof(int64_t) * R * comm->nranks), "cudaMalloc"));
+    std::vector<int64_t> all((size_t)R * comm->nranks);
+    iabn_status s = cuda(cudaMemcpyAsync(d + R * comm->rank, mine, sizeof(mine),
+                                         cudaMemcpyHostToDevice, st), "copy");
+    if (s == IABN_OK) {
+        const ncclResult_t r = n->AllGather(d + R * comm->rank, d, R, ncclInt64, comm->comm, st);
+        if (r != ncclSuccess) s = fail(IABN_ERR_NCCL, "ncclAllGather: %s", n->GetErrorString(r));
+    }
+    if (s == IABN_OK)
+        s = cuda(cudaMemcpyAsync(all.data(), d, sizeof(int64_t) * all.size(), cudaMemcpyDeviceToHost,
+                                 st), "copy");
+    if (s == IABN_OK) s = cuda(cudaStreamSynchronize(st), "stream synchronize");
+    cudaFree(d);
+    IABN_TRY(s);
+    SyncAgree a{g.N, g.C, g.HW, (int)g.dtype, (int)g.layout, pass, true, 0};
+    for (int r = 0; r < comm->nranks; ++r) {
+        const int64_t* o = &all[(size_t)R * r];
+        a.m_global += o[0] * o[2];
+        if (!o[4] || memcmp(o, mine, sizeof(mine)) != 0) a.fused = false;
+    }
+    comm->agree.push_back(a);
+    *out = a;
+    return IABN_OK;
 }
 
 // ====================================================================== shared call bodies
@@ -1227,9 +1307,9 @@ iabn_status emu_sync_buf(cudaStream_t st, int G, int64_t C, SyncBuf* out) {
     if (cudaMalloc(&base, bytes) != cudaSuccess)
         return fail(IABN_ERR_CUDA, "exchange buffers (%zu bytes): %s", bytes,
                     cudaGetErrorString(cudaGetLastError()));
-    const unsigned long long init[2] = {1ull, 0ull};
-    if (cudaMemset(base, 0, bytes) != cudaSuccess ||
-        cudaMemcpy(base, init, sizeof(init), cudaMemcpyHostToDevice) != cudaSuccess) {
+    static const unsigned long long init[2] = {1ull, 0ull};
+    if (cudaMemsetAsync(base, 0, bytes, st) != cudaSuccess ||
+        cudaMemcpyAsync(base, init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess) {
         cudaFree(base);
         return fail(IABN_ERR_CUDA, "exchange buffers init: %s", cudaGetErrorString(cudaGetLastError()));
     }
@@ -1391,6 +1471,35 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                             beta, sv, dg, db, eps, slope, flags);
 }
 
+// ====================================================================== fault injection
+// Test-of-tests only (iabn_debug_fault, not in include/iabn.h): perturb one output of
+// every call by a relative 1e-3 so that the GPU parity harness can be shown to fail.
+std::atomic<uint32_t> g_fault{0};
+enum : uint32_t { FAULT_DGAMMA = 1, FAULT_Z = 2, FAULT_DX = 4, FAULT_RUNNING_VAR = 8 };
+
+__global__ void fault_scale_kernel(float* v, int64_t n) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[i] *= 1.001f;
+}
+__global__ void fault_act_kernel(void* a, int dtype) {
+    if (dtype == IABN_F32) {
+        float* f = (float*)a;
+        f[0] = f[0] * 1.001f + 1e-3f;
+    } else {
+        __nv_bfloat16* h = (__nv_bfloat16*)a;  // bf16 tolerance is 2e-2: a larger step
+        const float v = __bfloat162float(h[0]);
+        h[0] = __float2bfloat16(v + 0.25f * fabsf(v) + 0.5f);
+    }
+}
+iabn_status fault_after(iabn_status s, int dtype, void* act, float* vec, int64_t n, uint32_t vbit,
+                        uint32_t abit, void* stream) {
+    const uint32_t f = g_fault.load(std::memory_order_relaxed);
+    if (s != IABN_OK || !f) return s;
+    const cudaStream_t st = (cudaStream_t)stream;
+    if ((f & vbit) && vec) fault_scale_kernel<<<1, 256, 0, st>>>(vec, n);
+    if ((f & abit) && act) fault_act_kernel<<<1, 1, 0, st>>>(act, dtype);
+    return check_launch("fault injection");
+}
+
 #define DISPATCH(dtype, fn, ...) \
     ((dtype) == IABN_F32 ? fn<float>(__VA_ARGS__) : fn<__nv_bfloat16>(__VA_ARGS__))
 
@@ -1429,6 +1538,10 @@ IABN_API size_t iabn_debug_trace(unsigned long long* host, size_t n) {
 }
 IABN_API uint32_t iabn_debug_trace_channels(void) { return g_trace_ch; }
 
+// Test-of-tests only (not in include/iabn.h): 1 = dgamma x 1.001, 2 = z[0] perturbed,
+// 4 = dx[0] perturbed, 8 = running_var x 1.001 on every later call; 0 = off.
+IABN_API void iabn_debug_fault(uint32_t mask) { g_fault.store(mask); }
+
 size_t iabn_workspace_bytes(const iabn_desc* desc) {
     Geom g;
     if (make_geom(desc, &g) != IABN_OK) return 0;
@@ -1465,8 +1578,9 @@ iabn_status iabn_forward(const iabn_desc* desc, const void* x, void* z, const fl
     IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
                           momentum, eps, slope, flags, c.g.m));
     IABN_TRY(attach_device(c));
-    return DISPATCH(c.g.dtype, forward_impl, c, x, z, gamma, beta, running_mean, running_var,
-                    save_mean, save_var, momentum, eps, slope, flags);
+    return fault_after(DISPATCH(c.g.dtype, forward_impl, c, x, z, gamma, beta, running_mean,
+                                running_var, save_mean, save_var, momentum, eps, slope, flags),
+                       c.g.dtype, z, running_var, c.g.C, FAULT_RUNNING_VAR, FAULT_Z, stream);
 }
 
 iabn_status iabn_backward(const iabn_desc* desc, const void* z, const void* dz, void* dx,
@@ -1478,8 +1592,9 @@ iabn_status iabn_backward(const iabn_desc* desc, const void* z, const void* dz, 
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
     IABN_TRY(attach_device(c));
-    return DISPATCH(c.g.dtype, backward_impl, c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta,
-                    eps, slope, flags);
+    return fault_after(DISPATCH(c.g.dtype, backward_impl, c, z, dz, dx, gamma, beta, save_var,
+                                dgamma, dbeta, eps, slope, flags),
+                       c.g.dtype, dx, dgamma, c.g.C, FAULT_DGAMMA, FAULT_DX, stream);
 }
 
 // ---------------------------------------------------------------- test time
@@ -1617,8 +1732,35 @@ iabn_status iabn_comm_destroy(iabn_comm comm) {
         cudaFree(comm->own);
     }
     if (comm->sb.ctr) cudaFree(comm->sb.ctr);
+    for (auto& pe : comm->ev)
+        for (cudaEvent_t e : pe)
+            if (e) cudaEventDestroy(e);
     delete comm;
     return s;
+}
+
+iabn_status iabn_comm_set_timing(iabn_comm comm, int on) {
+    if (!comm) return fail(IABN_ERR_INVALID_ARG, "comm is NULL");
+    comm->timing = on != 0;
+    comm->timed[0] = comm->timed[1] = false;
+    return IABN_OK;
+}
+
+iabn_status iabn_comm_phase_ms(iabn_comm comm, float ms[6]) {
+    if (!comm || !ms) return fail(IABN_ERR_INVALID_ARG, "NULL argument");
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int k = 0; k < 3; ++k) ms[3 * pass + k] = -1.f;
+        if (!comm->timed[pass]) continue;
+        const cudaError_t e = cudaEventSynchronize(comm->ev[pass][3]);
+        if (e != cudaSuccess) return fail(IABN_ERR_CUDA, "cudaEventSynchronize: %s", cudaGetErrorString(e));
+        for (int k = 0; k < 3; ++k) {
+            float t = 0.f;
+            if (cudaEventElapsedTime(&t, comm->ev[pass][k], comm->ev[pass][k + 1]) != cudaSuccess)
+                return fail(IABN_ERR_CUDA, "cudaEventElapsedTime failed");
+            ms[3 * pass + k] = t;
+        }
+    }
+    return IABN_OK;
 }
 
 iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, const float* gamma,
@@ -1637,24 +1779,37 @@ iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, con
                           momentum, eps, slope, flags, c.g.m * comm->nranks));
     IABN_TRY(attach_device(c));
     if (sync_fused_wanted(flags)) {
-        // channel-resident kernel with the exchange inside (every rank: the same desc)
+        // channel-resident kernel with the exchange inside, if every rank can run it with
+        // the same plan (else every rank takes the all-reduce path below)
         const FusedPlan p = fused_plan(c.g, 0, *c.dev, flags);
-        if (p.ok) {
+        SyncAgree ag;
+        IABN_TRY(sync_agree(comm, c.g, 0, p, c.st, &ag));
+        if (ag.fused) {
             IABN_TRY(comm_sync_buf(comm, c.g.C, c.st));
             FusedArgs a = fused_fwd_args(c.g, x, z, gamma, beta, running_mean, running_var,
                                          save_mean, save_var, momentum, eps, slope, flags);
             set_sync(a, comm->sb, 1, comm->nranks, comm->rank, (uint32_t)p.clusters, 0, 0.0);
-            return DISPATCH(c.g.dtype, launch_fused, 0, p, a, c.st);
+            phase_mark(comm, 0, 0, c.st);
+            IABN_TRY(DISPATCH(c.g.dtype, launch_fused, 0, p, a, c.st));
+            for (int k = 1; k <= 3; ++k) phase_mark(comm, 0, k, c.st);
+            return fault_after(IABN_OK, c.g.dtype, z, running_var, c.g.C, FAULT_RUNNING_VAR,
+                               FAULT_Z, stream);
         }
     }
     double* stats = wsp<double>(c, c.w.stats);
+    phase_mark(comm, 0, 0, c.st);
     IABN_TRY(DISPATCH(c.g.dtype, fwd_stream_stats, c, x));
     launch_pdl(combine_kernel<3>, wgrid(c.g.C), 128, 0, c.st, wsp<double>(c, c.w.part), c.S, c.g.C, stats,
                                                       -1.0);
     IABN_TRY(check_launch("combine kernel"));
+    phase_mark(comm, 0, 1, c.st);
     IABN_TRY(allreduce_f64(stats, (size_t)c.g.C * 3, comm, c.st));
-    return DISPATCH(c.g.dtype, fwd_from_partials, c, stats, 1, x, z, gamma, beta, running_mean,
-                    running_var, save_mean, save_var, momentum, eps, slope, flags);
+    phase_mark(comm, 0, 2, c.st);
+    IABN_TRY(DISPATCH(c.g.dtype, fwd_from_partials, c, stats, 1, x, z, gamma, beta, running_mean,
+                      running_var, save_mean, save_var, momentum, eps, slope, flags));
+    phase_mark(comm, 0, 3, c.st);
+    return fault_after(IABN_OK, c.g.dtype, z, running_var, c.g.C, FAULT_RUNNING_VAR, FAULT_Z,
+                       stream);
 }
 
 iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void* dz, void* dx,
@@ -1672,18 +1827,25 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
     IABN_TRY(attach_device(c));
     if (sync_fused_wanted(flags)) {
         const FusedPlan p = fused_plan(c.g, 1, *c.dev, flags);
-        if (p.ok) {
+        SyncAgree ag;
+        IABN_TRY(sync_agree(comm, c.g, 1, p, c.st, &ag));
+        if (ag.fused) {
             IABN_TRY(comm_sync_buf(comm, c.g.C, c.st));
             FusedArgs a = fused_bwd_args(c.g, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps,
                                          slope, flags);
             set_sync(a, comm->sb, 1, comm->nranks, comm->rank, (uint32_t)p.clusters, 0,
-                     1.0 / ((double)c.g.m * comm->nranks));
-            return DISPATCH(c.g.dtype, launch_fused, 1, p, a, c.st);
+                     1.0 / (double)ag.m_global);
+            phase_mark(comm, 1, 0, c.st);
+            IABN_TRY(DISPATCH(c.g.dtype, launch_fused, 1, p, a, c.st));
+            for (int k = 1; k <= 3; ++k) phase_mark(comm, 1, k, c.st);
+            return fault_after(IABN_OK, c.g.dtype, dx, dgamma, c.g.C, FAULT_DGAMMA, FAULT_DX,
+                               stream);
         }
     }
     double* part = wsp<double>(c, c.w.part);
     double* loc = wsp<double>(c, c.w.sums_loc);
     double* glob = wsp<double>(c, c.w.sums_glob);
+    phase_mark(comm, 1, 0, c.st);
     IABN_TRY(DISPATCH(c.g.dtype, launch_bwd_reduce, c.g, c.S, z, dz, gamma, beta, eps, slope,
                       flags, part, c.st));
     launch_pdl(combine_kernel<2>, wgrid(c.g.C), 128, 0, c.st, part, c.S, c.g.C, loc, (double)c.g.m);
@@ -1691,10 +1853,14 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
     const size_t nb = (size_t)(2 * c.g.C + 1) * sizeof(double);
     const cudaError_t e = cudaMemcpyAsync(glob, loc, nb, cudaMemcpyDeviceToDevice, c.st);
     if (e != cudaSuccess) return fail(IABN_ERR_CUDA, "cudaMemcpyAsync: %s", cudaGetErrorString(e));
+    phase_mark(comm, 1, 1, c.st);
     IABN_TRY(allreduce_f64(glob, (size_t)(2 * c.g.C + 1), comm, c.st));
+    phase_mark(comm, 1, 2, c.st);
     const double* lsrc = (flags & IABN_SYNC_GLOBAL_PARAM_GRADS) ? glob : loc;
-    return DISPATCH(c.g.dtype, bwd_from_sums, c, glob, 1, lsrc, 1, glob + 2 * c.g.C, 0.0, z, dz,
-                    dx, gamma, beta, save_var, dgamma, dbeta, eps, slope, flags);
+    IABN_TRY(DISPATCH(c.g.dtype, bwd_from_sums, c, glob, 1, lsrc, 1, glob + 2 * c.g.C, 0.0, z, dz,
+                      dx, gamma, beta, save_var, dgamma, dbeta, eps, slope, flags));
+    phase_mark(comm, 1, 3, c.st);
+    return fault_after(IABN_OK, c.g.dtype, dx, dgamma, c.g.C, FAULT_DGAMMA, FAULT_DX, stream);
 }
 
 // ---------------------------------------------------------------- one-GPU emulation
@@ -1734,7 +1900,8 @@ iabn_status iabn_forward_sync_emulated(const iabn_desc* desc, int nranks, const 
                                  save_var, momentum, eps, slope, flags);
     const uint32_t qv = (uint32_t)std::min<int64_t>(gl.C, p.max_clusters / nranks);
     set_sync(a, sb, nranks, nranks, 0, qv, gl.E, 0.0);
-    return DISPATCH(gl.dtype, launch_fused, 0, p, a, c.st);
+    return fault_after(DISPATCH(gl.dtype, launch_fused, 0, p, a, c.st), gl.dtype, z, running_var,
+                       gl.C, FAULT_RUNNING_VAR, FAULT_Z, stream);
 }
 
 iabn_status iabn_backward_sync_emulated(const iabn_desc* desc, int nranks, const void* z,
@@ -1758,7 +1925,8 @@ iabn_status iabn_backward_sync_emulated(const iabn_desc* desc, int nranks, const
                                  flags);
     const uint32_t qv = (uint32_t)std::min<int64_t>(gl.C, p.max_clusters / nranks);
     set_sync(a, sb, nranks, nranks, 0, qv, gl.E, 1.0 / ((double)gl.m * nranks));
-    return DISPATCH(gl.dtype, launch_fused, 1, p, a, c.st);
+    return fault_after(DISPATCH(gl.dtype, launch_fused, 1, p, a, c.st), gl.dtype, dx, dgamma,
+                       gl.C * nranks, FAULT_DGAMMA, FAULT_DX, stream);
 }
 
 }  // extern "C"

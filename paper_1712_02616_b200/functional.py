@@ -152,6 +152,19 @@ class Comm:
         uid = broadcast_unique_id(group, cls.unique_id)
         return cls.create(dist.get_world_size(group), dist.get_rank(group), uid)
 
+    def set_timing(self, on: bool = True) -> None:
+        """Record per-phase CUDA events in the synchronized calls (iabn_comm_set_timing)."""
+        L.call("iabn_comm_set_timing", self.handle, 1 if on else 0)
+
+    def phase_ms(self) -> dict:
+        """Device time of the last timed forward / backward, per phase (iabn_comm_phase_ms):
+        {"forward": {"reduce", "allreduce", "apply"}, "backward": {...}} in ms."""
+        buf = (ctypes.c_float * 6)()
+        L.call("iabn_comm_phase_ms", self.handle, buf)
+        names = ("reduce", "allreduce", "apply")
+        return {p: {n: float(buf[3 * i + k]) for k, n in enumerate(names)}
+                for i, p in enumerate(("forward", "backward"))}
+
     def close(self) -> None:
         if self.handle:
             L.call("iabn_comm_destroy", self.handle)

@@ -97,3 +97,28 @@ CONFIGS = {
 RX101_LAYERS = [(64, 112 * 112, 1), (64, 56 * 56, 1), (128, 56 * 56, 6), (256, 56 * 56, 4),
                 (256, 28 * 28, 7), (512, 28 * 28, 5), (512, 14 * 14, 45), (1024, 14 * 14, 24),
                 (1024, 7 * 7, 5), (2048, 7 * 7, 3)]
+
+
+def densenet264_layers() -> list[tuple[int, int]]:
+    """(C, HW) of every BN of DenseNet-BC-264 (growth 32, blocks 6/12/64/48, bottleneck
+    4*32) at 224^2, in network order: stem BN, per dense layer BN(concat) + BN(128),
+    transition BNs, final BN (C 64..2688)."""
+    k, out = 32, [(64, 112 * 112)]
+    c, hw = 64, 56 * 56
+    for bi, n in enumerate((6, 12, 64, 48)):
+        for i in range(n):
+            out.append((c + i * k, hw))
+            out.append((4 * k, hw))
+        c += n * k
+        if bi < 3:
+            out.append((c, hw))  # transition BN
+            c //= 2
+            hw //= 4
+    out.append((c, hw))  # final BN
+    return out
+
+
+def rx101_layers() -> list[tuple[int, int]]:
+    """(C, HW) of the 101 BN+Act layers of ResNeXt-101 32x4d in network order."""
+    return [(c, hw) for c, hw, n in RX101_LAYERS for _ in range(n)]
+

@@ -124,3 +124,16 @@ def compare(case: Case, got, ref, p, *, tol=None):
     bad = {k: v for k, v in errs.items() if k != "n_ambiguous" and not (v <= tol)}
     assert not bad, f"parity failed ({case}): {errs}"
     return errs
+
+
+def shard_param_errs(case: Case, ref, amb, sl: slice, got_dg, got_db, exp_dg, exp_db) -> dict:
+    """Normwise errors of one shard's dgamma / dbeta (samples ``sl`` of the concatenated
+    batch) with the R16 allowance of that shard's ambiguous activation branches."""
+    a = amb[sl]
+    allow = (1 - case.slope) * np.abs(ref["dz"][sl]) * (2.0 + np.abs(ref["y"][sl])) * a
+    allow = allow.sum(axis=tuple(i for i in range(3) if i != case.ax))
+    out = {}
+    for k, got, exp in (("dgamma", got_dg, exp_dg), ("dbeta", got_db, exp_db)):
+        d = np.maximum(np.abs(np.asarray(got, dtype=np.float64) - exp) - allow, 0.0)
+        out[k] = float(d.max() / max(np.abs(exp).max(), 1e-30))
+    return out

@@ -478,9 +478,12 @@ def test_grid_resident_matches_streaming_bitwise_stats():
 @pytest.mark.parametrize("case", [Case(4, 24, 196, dtype="f32", seed=52),
                                   Case(4, 40, 64, dtype="bf16", layout="NHWC", seed=53)],
                          ids=["nchw_f32", "nhwc_bf16"])
-def test_sync_through_nccl_single_rank(case):
-    """iabn_forward_sync / iabn_backward_sync with a real NCCL communicator of one rank
-    (the all-reduce runs; results equal the oracle on the batch)."""
+def test_sync_entry_points_single_rank(case):
+    """iabn_forward_sync / iabn_backward_sync with a real NCCL communicator of ONE rank:
+    communicator setup and teardown, and the one-rank shortcut (nranks == 1 takes the
+    non-synchronized path, no all-reduce) match the oracle.  The all-reduce path itself
+    (nranks >= 2) is tests/test_sync_shim_gpu.py (and tests/test_sync_multigpu.py on a
+    multi-GPU box)."""
     import paper_1712_02616_b200 as P
     comm = P.Comm.create(1, 0, P.Comm.unique_id())
     try:

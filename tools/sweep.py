@@ -24,27 +24,8 @@ import synth_inputs as S  # noqa: E402
 from paper_1712_02616_b200 import _lib as L  # noqa: E402
 
 
-def densenet264_layers():
-    """(C, HW) of every BN of DenseNet-BC-264 (growth 32, blocks 6/12/64/48, bottleneck
-    4*32) at 224^2, in network order: stem BN, per dense layer BN(concat) + BN(128),
-    transition BNs, final BN (C up to 2688)."""
-    k, out = 32, [(64, 112 * 112)]
-    c, hw = 64, 56 * 56
-    for bi, n in enumerate((6, 12, 64, 48)):
-        for i in range(n):
-            out.append((c + i * k, hw))
-            out.append((4 * k, hw))
-        c += n * k
-        if bi < 3:
-            out.append((c, hw))  # transition BN
-            c //= 2
-            hw //= 4
-    out.append((c, hw))  # final BN
-    return out
-
-
-def rx101_layers():
-    return [(c, hw) for c, hw, n in S.RX101_LAYERS for _ in range(n)]
+densenet264_layers = S.densenet264_layers
+rx101_layers = S.rx101_layers
 
 
 def main():
