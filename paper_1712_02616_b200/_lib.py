@@ -27,7 +27,6 @@ EVAL = 1 << 4
 VARIANT_I = 1 << 5
 FORCE_STREAMING = 1 << 8
 FORCE_FUSED = 1 << 9
-FORCE_ONE_LAUNCH = 1 << 10
 FORCE_RESIDENT = 1 << 11
 SYNC_FUSED = 1 << 12
 

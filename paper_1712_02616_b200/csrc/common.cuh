@@ -85,17 +85,19 @@ __device__ __forceinline__ void st_scalar<__nv_bfloat16>(__nv_bfloat16* p, float
     *p = __float2bfloat16_rn(v);
 }
 
-// 16-byte global accesses.  Loads of data touched once per kernel use the
-// non-coherent path without L1 allocation; stores are plain (write-back L2).
+// 16-byte global accesses, no L1 allocation (data touched once per kernel); stores are
+// plain (write-back L2).  ld_vec is the coherent load: the apply kernels use it on
+// buffers the same kernel overwrites (z over x, dx over dz in place), which the
+// read-only .nc path does not allow.
 __device__ __forceinline__ uint4 ld_vec(const void* p) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
 }
-// Same load, not volatile: the compiler may batch and hoist it (inputs that no thread
-// of the kernel writes).
+// Non-coherent read-only load, not volatile (the compiler may batch and hoist it): only
+// for inputs that no thread of the kernel writes (the reduction kernels).
 __device__ __forceinline__ uint4 ld_vec_ro(const void* p) {
     uint4 r;
     asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"

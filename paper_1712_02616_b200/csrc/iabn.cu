@@ -22,7 +22,6 @@
 #include <string>
 
 #include "iabn.h"
-#include "kernels_coop.cuh"
 #include "kernels_gres.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_stream.cuh"
@@ -615,69 +614,6 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     return check_launch(pass == 0 ? "fused_kernel<fwd>" : "fused_kernel<bwd>");
 }
 
-// ====================================================================== one-launch schedule
-// Small layers (the whole input a few tens of MB, so its second read hits L2):
-// the streaming phases in one cooperative launch (kernels_coop.cuh).
-size_t coop_max_bytes() {
-    static const size_t mb = (size_t)std::max(0, env_int("IABN_COOP_MB", 48)) << 20;
-    return mb;
-}
-// Opt-in (IABN_FORCE_ONE_LAUNCH, or env IABN_COOP=1 for small layers the fused
-// schedule cannot take): measured slower than the three streaming launches on
-// B200 for every sweep shape (profiles/r01_sweep_*; the grid barriers and the
-// lower occupancy cost more than the two launches they save), so not a default.
-bool coop_wanted(const Geom& g, int pass, uint32_t flags, bool fused_ok) {
-    if (flags & IABN_FORCE_STREAMING) return false;
-    if (flags & IABN_FORCE_ONE_LAUNCH) return true;
-    if (flags & IABN_FORCE_FUSED) return false;
-    if (env_int("IABN_COOP", 0) != 1) return false;
-    const size_t bytes = (size_t)g.E * g.b * (pass == 0 ? 1 : 2);
-    return !fused_ok && bytes <= coop_max_bytes();
-}
-
-template <typename T, int LAYOUT, bool VEC, int PASS>
-iabn_status launch_coop_t(const Geom& g, CoopArgs a, cudaStream_t st, int sms) {
-    const void* fn = (const void*)coop_kernel<T, LAYOUT, VEC, PASS>;
-    static int occ = -1;  // per instantiation (same on every B200)
-    if (occ < 0) {
-        int o = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, kThreads, 0) != cudaSuccess) {
-            cudaGetLastError();
-            o = 0;
-        }
-        occ = o;
-    }
-    if (occ <= 0) return fail(IABN_ERR_UNSUPPORTED, "one-launch kernel cannot be resident");
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(occ * sms), 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, coop_kernel<T, LAYOUT, VEC, PASS>, a);
-    if (e != cudaSuccess) {
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        return fail(IABN_ERR_CUDA, "one-launch kernel: %s", cudaGetErrorString(e));
-    }
-    return check_launch(PASS == 0 ? "coop_kernel<fwd>" : "coop_kernel<bwd>");
-}
-
-template <typename T, int PASS>
-iabn_status launch_coop(const Geom& g, CoopArgs a, cudaStream_t st, int sms) {
-    if (cudaMemsetAsync(a.bar, 0, sizeof(unsigned), st) != cudaSuccess)
-        return fail(IABN_ERR_CUDA, "barrier reset: %s", cudaGetErrorString(cudaGetLastError()));
-    const bool vec = vec_ok(g);
-    if (g.layout == IABN_NCHW)
-        return vec ? launch_coop_t<T, 0, true, PASS>(g, a, st, sms)
-                   : launch_coop_t<T, 0, false, PASS>(g, a, st, sms);
-    return vec ? launch_coop_t<T, 1, true, PASS>(g, a, st, sms)
-               : launch_coop_t<T, 1, false, PASS>(g, a, st, sms);
-}
-
-// covering vectors per plane of the misaligned NCHW reductions (nchw_cover_body)
 FastDiv cover_fd(const Geom& g) { return make_fastdiv((uint32_t)(g.HW / (16 / g.b) + 2)); }
 
 // ====================================================================== grid-resident NHWC
@@ -686,7 +622,7 @@ FastDiv cover_fd(const Geom& g) { return make_fastdiv((uint32_t)(g.HW / (16 / g.
 // IABN_GRES_KB (default 96) KB of input each, 2 CTAs per SM, G <= kGresMaxG.
 int gres_grid(const Geom& g, int pass, uint32_t flags, const DevFacts& f) {
     if (g.layout != IABN_NHWC || !vec_ok(g) || g.E >= (1ll << 31)) return 0;
-    if (flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_ONE_LAUNCH | IABN_EVAL))
+    if (flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_EVAL))
         return 0;
     // opt-in: measured against the streaming kernels (tools/shape_graph.py, graph replay,
     // DenseNet-like NHWC shapes at N = 32) it wins for bf16 layers of ~13 MB (1.1-1.4x)
@@ -1333,7 +1269,7 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
     }
     FusedPlan p;
-    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 0, *c.dev, flags);
+    if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 0, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shape");
     if (p.ok)
@@ -1358,33 +1294,6 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
                             flags};
         return launch_gres<T, 0>(c.g, G, a, c.st);
     }
-    if (coop_wanted(c.g, 0, flags, false) && c.g.E < (1ll << 31)) {
-        CoopArgs a{};
-        a.in0 = x;
-        a.out = z;
-        a.C = c.g.C;
-        a.HW = c.g.HW;
-        a.rows = c.g.m;
-        a.m = (uint32_t)c.g.m;
-        a.E = (uint32_t)c.g.E;
-        a.fd_hw = fd32(c.g.HW);
-        a.fd_c = fd32(c.g.C);
-        a.fd_cover = cover_fd(c.g);
-        a.N = c.g.N;
-        a.S = c.S;
-        a.part = wsp<double>(c, c.w.part);
-        a.coef = wsp<float4>(c, c.w.coef);
-        a.bar = wsp<unsigned>(c, c.w.bar);
-        a.slope = slope;
-        a.inv_slope = 1.0f / slope;
-        a.eps = eps;
-        a.flags = flags;
-        a.fwd = FwdCoefArgs{a.part, c.S, c.g.C, gamma, beta, rm, rv, sm, sv, a.coef, momentum,
-                            eps, flags};
-        return launch_coop<T, 0>(c.g, a, c.st, c.dev->sms);
-    }
-    if (flags & IABN_FORCE_ONE_LAUNCH)
-        return fail(IABN_ERR_UNSUPPORTED, "one-launch schedule needs fewer than 2^31 elements");
     IABN_TRY(fwd_stream_stats<T>(c, x));
     return fwd_from_partials<T>(c, wsp<double>(c, c.w.part), c.S, x, z, gamma, beta, rm, rv, sm,
                                 sv, momentum, eps, slope, flags);
@@ -1407,7 +1316,7 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                           const float* gamma, const float* beta, const float* sv, float* dg,
                           float* db, float eps, float slope, uint32_t flags) {
     FusedPlan p;
-    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_ONE_LAUNCH))) p = fused_plan(c.g, 1, *c.dev, flags);
+    if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 1, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shape");
     if (p.ok)
@@ -1436,36 +1345,6 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                             db, a.coef, eps, flags};
         return launch_gres<T, 1>(c.g, G, a, c.st);
     }
-    if (coop_wanted(c.g, 1, flags, false) && c.g.E < (1ll << 31)) {
-        CoopArgs a{};
-        a.in0 = z;
-        a.in1 = dz;
-        a.out = dx;
-        a.C = c.g.C;
-        a.HW = c.g.HW;
-        a.rows = c.g.m;
-        a.m = (uint32_t)c.g.m;
-        a.E = (uint32_t)c.g.E;
-        a.fd_hw = fd32(c.g.HW);
-        a.fd_c = fd32(c.g.C);
-        a.fd_cover = cover_fd(c.g);
-        a.N = c.g.N;
-        a.S = c.S;
-        a.part = part;
-        a.coef = wsp<float4>(c, c.w.coef);
-        a.bar = wsp<unsigned>(c, c.w.bar);
-        a.slope = slope;
-        a.inv_slope = 1.0f / slope;
-        a.eps = eps;
-        a.flags = flags;
-        a.gamma = gamma;
-        a.beta = beta;
-        a.bwd = BwdCoefArgs{part, c.S, part, c.S, nullptr, (double)c.g.m, c.g.C, gamma, beta,
-                            sv, dg, db, a.coef, eps, flags};
-        return launch_coop<T, 1>(c.g, a, c.st, c.dev->sms);
-    }
-    if (flags & IABN_FORCE_ONE_LAUNCH)
-        return fail(IABN_ERR_UNSUPPORTED, "one-launch schedule needs fewer than 2^31 elements");
     IABN_TRY(launch_bwd_reduce<T>(c.g, c.S, z, dz, gamma, beta, eps, slope, flags, part, c.st));
     return bwd_from_sums<T>(c, part, c.S, part, c.S, nullptr, (double)c.g.m, z, dz, dx, gamma,
                             beta, sv, dg, db, eps, slope, flags);
@@ -1559,12 +1438,10 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     DevFacts* dev;
     IABN_TRY(device_facts(&dev));
     FusedPlan p;
-    if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_ONE_LAUNCH)))
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL)))
         p = fused_plan(g, pass, *dev, flags);
     *schedule = p.ok ? 1 : 0;
     *cluster = p.ok ? p.K : 0;
-    if (!p.ok && !(flags & IABN_EVAL) && g.E < (1ll << 31) && coop_wanted(g, pass, flags, false))
-        *schedule = 2;
     if (!p.ok && *schedule == 0 && gres_grid(g, pass, flags, *dev) > 0) *schedule = 3;
     return IABN_OK;
 }

@@ -77,12 +77,26 @@ def workspace(d: L.Desc, device: torch.device, stream=None) -> tuple[int, int]:
     nbytes = _WSB.get(dk)
     if nbytes is None:
         nbytes = _WSB[dk] = max(L.workspace_bytes(d), 16)
-    key = (device.index, _stream(stream))
+    key = (device.index, _stream(stream, device))
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
-        ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        if stream is None:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        else:
+            # allocated from the explicit stream's pool: when it is later replaced, the
+            # caching allocator reuses it only after the work queued on that stream
+            with torch.cuda.stream(stream):
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws.data_ptr(), ws.numel()
+
+
+def _empty_c(C: int, device: torch.device, stream) -> torch.Tensor:
+    """A per-channel fp32 output, allocated on the stream the kernels write it from."""
+    if stream is None:
+        return torch.empty(C, dtype=torch.float32, device=device)
+    with torch.cuda.stream(stream):
+        return torch.empty(C, dtype=torch.float32, device=device)
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -101,12 +115,15 @@ _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
 _CUR_DEV = getattr(torch._C, "_cuda_getDevice", None)
 
 
-def _stream(stream) -> int:
+def _stream(stream, device: torch.device | None = None) -> int:
+    """The CUDA stream handle of a call: the explicit one, else the current stream of the
+    tensors' device (not of the current device)."""
     if stream is not None:
         return stream.cuda_stream
-    if _RAW_STREAM is not None and _CUR_DEV is not None:  # same value, without the Stream object
-        return _RAW_STREAM(_CUR_DEV())
-    return torch.cuda.current_stream().cuda_stream
+    idx = device.index if device is not None and device.index is not None else None
+    if _RAW_STREAM is not None:  # same value, without building a Stream object
+        return _RAW_STREAM(idx if idx is not None else _CUR_DEV())
+    return torch.cuda.current_stream(idx).cuda_stream
 
 
 def _flags(gamma_mode: str, running_var_biased: bool = False, extra: int = 0) -> int:
@@ -189,14 +206,14 @@ def forward(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
     running_var = _f32(running_var, C, "running_var")
     fl = _flags(gamma_mode, running_var_biased, flags) | (0 if training else L.EVAL)
     if training:
-        save_mean = torch.empty(C, dtype=torch.float32, device=x.device)
-        save_var = torch.empty(C, dtype=torch.float32, device=x.device)
+        save_mean = _empty_c(C, x.device, stream)
+        save_var = _empty_c(C, x.device, stream)
     else:
         save_mean = save_var = None
     ws, nb = workspace(d, x.device, stream)
     args = [ctypes.byref(d), x.data_ptr(), z.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
             _ptr(running_mean), _ptr(running_var), _ptr(save_mean), _ptr(save_var), momentum, eps,
-            slope, fl, ws, nb, _stream(stream)]
+            slope, fl, ws, nb, _stream(stream, x.device)]
     if comm is None:
         L.call("iabn_forward", *args)
     else:
@@ -209,8 +226,9 @@ def backward(z: torch.Tensor, dz: torch.Tensor, gamma: torch.Tensor, beta: torch
              slope: float = 0.01, dx: torch.Tensor | None = None, gamma_mode: str = "abs_eps",
              layout: str = "NCHW", flags: int = 0, comm: Comm | None = None,
              global_param_grads: bool = False, stream=None):
-    """Alg. 2 (variant I): from z and dL/dz only.  dx is written over dz unless
-    ``dx`` is given.  Returns (dx, dgamma, dbeta)."""
+    """Alg. 2: from z and dL/dz only (variant II / BN-dagger in the channel-resident
+    kernels, I in the streaming ones and with IABN_VARIANT_I; R6).  dx is
+    written over dz unless ``dx`` is given.  Returns (dx, dgamma, dbeta)."""
     d = _desc(z, layout)
     C = d.c
     if dz.shape != z.shape or dz.dtype != z.dtype or not dz.is_contiguous():
@@ -218,13 +236,13 @@ def backward(z: torch.Tensor, dz: torch.Tensor, gamma: torch.Tensor, beta: torch
     dx = dz if dx is None else dx
     gamma, beta = _f32(gamma, C, "gamma"), _f32(beta, C, "beta")
     save_var = _f32(save_var, C, "save_var")
-    dgamma = torch.empty(C, dtype=torch.float32, device=z.device)
-    dbeta = torch.empty(C, dtype=torch.float32, device=z.device)
+    dgamma = _empty_c(C, z.device, stream)
+    dbeta = _empty_c(C, z.device, stream)
     fl = _flags(gamma_mode, False, flags) | (L.SYNC_GLOBAL_PARAM_GRADS if global_param_grads else 0)
     ws, nb = workspace(d, z.device, stream)
     args = [ctypes.byref(d), z.data_ptr(), dz.data_ptr(), dx.data_ptr(), gamma.data_ptr(),
             beta.data_ptr(), _ptr(save_mean), save_var.data_ptr(), dgamma.data_ptr(),
-            dbeta.data_ptr(), eps, slope, fl, ws, nb, _stream(stream)]
+            dbeta.data_ptr(), eps, slope, fl, ws, nb, _stream(stream, z.device)]
     if comm is None:
         L.call("iabn_backward", *args)
     else:
@@ -259,7 +277,7 @@ def forward_sync_emulated(x: torch.Tensor, nranks: int, gamma: torch.Tensor, bet
     L.call("iabn_forward_sync_emulated", ctypes.byref(shard), nranks, x.data_ptr(), z.data_ptr(),
            gamma.data_ptr(), beta.data_ptr(), _ptr(running_mean), _ptr(running_var),
            save_mean.data_ptr(), save_var.data_ptr(), momentum, eps, slope,
-           _flags(gamma_mode, running_var_biased, flags), ws, nb, _stream(stream))
+           _flags(gamma_mode, running_var_biased, flags), ws, nb, _stream(stream, x.device))
     return z, save_mean, save_var
 
 
@@ -285,7 +303,7 @@ def backward_sync_emulated(z: torch.Tensor, dz: torch.Tensor, nranks: int, gamma
     L.call("iabn_backward_sync_emulated", ctypes.byref(shard), nranks, z.data_ptr(), dz.data_ptr(),
            dx.data_ptr(), _f32(gamma, C, "gamma").data_ptr(), _f32(beta, C, "beta").data_ptr(),
            None, _f32(save_var, C, "save_var").data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
-           eps, slope, fl, ws, nb, _stream(stream))
+           eps, slope, fl, ws, nb, _stream(stream, z.device))
     return dx, dgamma, dbeta
 
 
@@ -296,7 +314,7 @@ def forward_reduce(x: torch.Tensor, *, layout: str = "NCHW", stream=None) -> tor
     stats = torch.empty(d.c, 3, dtype=torch.float64, device=x.device)
     ws, nb = workspace(d, x.device, stream)
     L.call("iabn_forward_reduce", ctypes.byref(d), x.data_ptr(), stats.data_ptr(), ws, nb,
-           _stream(stream))
+           _stream(stream, x.device))
     return stats
 
 
@@ -316,7 +334,7 @@ def forward_apply(x: torch.Tensor, stats_global: torch.Tensor, gamma, beta, runn
            _f32(beta, C, "beta").data_ptr(), _ptr(_f32(running_mean, C, "running_mean")),
            _ptr(_f32(running_var, C, "running_var")), save_mean.data_ptr(), save_var.data_ptr(),
            momentum, eps, slope, _flags(gamma_mode, running_var_biased, flags), ws, nb,
-           _stream(stream))
+           _stream(stream, x.device))
     return z, save_mean, save_var
 
 
@@ -329,7 +347,7 @@ def backward_reduce(z, dz, gamma, beta, *, eps=1e-5, slope=0.01, gamma_mode="abs
     ws, nb = workspace(d, z.device, stream)
     L.call("iabn_backward_reduce", ctypes.byref(d), z.data_ptr(), dz.data_ptr(),
            _f32(gamma, C, "gamma").data_ptr(), _f32(beta, C, "beta").data_ptr(), sums.data_ptr(),
-           eps, slope, _flags(gamma_mode, False, flags), ws, nb, _stream(stream))
+           eps, slope, _flags(gamma_mode, False, flags), ws, nb, _stream(stream, z.device))
     return sums
 
 
@@ -346,7 +364,7 @@ def backward_apply(z, dz, sums_global, sums_local, gamma, beta, save_var, *, eps
     L.call("iabn_backward_apply", ctypes.byref(d), z.data_ptr(), dz.data_ptr(), dx.data_ptr(),
            sums_global.data_ptr(), _ptr(sums_local), _f32(gamma, C, "gamma").data_ptr(),
            _f32(beta, C, "beta").data_ptr(), _f32(save_var, C, "save_var").data_ptr(),
-           dgamma.data_ptr(), dbeta.data_ptr(), eps, slope, fl, ws, nb, _stream(stream))
+           dgamma.data_ptr(), dbeta.data_ptr(), eps, slope, fl, ws, nb, _stream(stream, z.device))
     return dx, dgamma, dbeta
 
 
@@ -369,7 +387,7 @@ def fold_conv(weight: torch.Tensor, bias: torch.Tensor | None, running_mean: tor
                                                                     device=weight.device)
     L.call("iabn_fold_conv", cout, kper, _ptr(weight), _ptr(bias), _ptr(running_mean),
            _ptr(running_var), _ptr(gamma), _ptr(beta), eps, _flags(gamma_mode), _ptr(w_out),
-           _ptr(b_out), _stream(stream))
+           _ptr(b_out), _stream(stream, weight.device))
     return w_out, b_out
 
 
@@ -385,40 +403,49 @@ class InPlaceABNFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, gamma, beta, running_mean, running_var, momentum, eps, slope, training,
-                gamma_mode, layout, comm):
+                gamma_mode, layout, comm, grad_inplace=True):
         z, _, save_var = forward(x, gamma.detach(), beta.detach(), running_mean, running_var,
                                  momentum=momentum, eps=eps, slope=slope, training=training,
                                  gamma_mode=gamma_mode, layout=layout, comm=comm)
         ctx.mark_dirty(x)
         ctx.save_for_backward(z, gamma, beta, save_var)
-        ctx.cfg = (eps, slope, gamma_mode, layout, comm, training)
+        ctx.cfg = (eps, slope, gamma_mode, layout, comm, training, grad_inplace)
         return z
 
     @staticmethod
     def backward(ctx, dz):
         z, gamma, beta, save_var = ctx.saved_tensors
-        eps, slope, gamma_mode, layout, comm, training = ctx.cfg
+        eps, slope, gamma_mode, layout, comm, training, grad_inplace = ctx.cfg
         if not training:
             raise RuntimeError("backward through eval-mode InPlace-ABN is not supported")
         dz = dz.contiguous()
+        # gradient sharing: dL/dx is written over dL/dz unless disabled
         dx, dgamma, dbeta = backward(z, dz, gamma.detach(), beta.detach(), save_var, eps=eps,
-                                     slope=slope, dx=torch.empty_like(dz), gamma_mode=gamma_mode,
-                                     layout=layout, comm=comm)
-        return dx, dgamma, dbeta, None, None, None, None, None, None, None, None, None
+                                     slope=slope, dx=None if grad_inplace else torch.empty_like(dz),
+                                     gamma_mode=gamma_mode, layout=layout, comm=comm)
+        return dx, dgamma, dbeta, None, None, None, None, None, None, None, None, None, None
 
 
 def inplace_abn(x, gamma, beta, running_mean=None, running_var=None, *, momentum=0.1, eps=1e-5,
-                slope=0.01, training=True, gamma_mode="abs_eps", layout="NCHW", comm=None):
+                slope=0.01, training=True, gamma_mode="abs_eps", layout="NCHW", comm=None,
+                grad_inplace=True):
+    """Autograd entry: z written over x (mark_dirty) and, with ``grad_inplace`` (default,
+    the paper's gradient sharing), dL/dx written over the incoming dL/dz.
+    The incoming gradient buffer is then consumed: pass ``grad_inplace=False`` if a
+    caller keeps its own reference to the gradient it feeds in (e.g. z.backward(g) with
+    a g it reuses)."""
     return InPlaceABNFunction.apply(x, gamma, beta, running_mean, running_var, momentum, eps,
-                                    slope, training, gamma_mode, layout, comm)
+                                    slope, training, gamma_mode, layout, comm, grad_inplace)
 
 
 class InPlaceABN(torch.nn.Module):
     """The plug-in BN+LeakyReLU layer of PAPER.md:200 (fp32 gamma/beta, running stats)."""
 
     def __init__(self, num_features: int, *, eps=1e-5, momentum=0.1, slope=0.01,
-                 gamma_mode="abs_eps", comm: Comm | None = None, device=None):
+                 gamma_mode="abs_eps", comm: Comm | None = None, device=None,
+                 grad_inplace: bool = True):
         super().__init__()
+        self.grad_inplace = grad_inplace
         self.weight = torch.nn.Parameter(torch.ones(num_features, device=device))
         self.bias = torch.nn.Parameter(torch.zeros(num_features, device=device))
         self.register_buffer("running_mean", torch.zeros(num_features, device=device))
@@ -432,5 +459,5 @@ class InPlaceABN(torch.nn.Module):
         z = inplace_abn(xs, self.weight, self.bias, self.running_mean, self.running_var,
                         momentum=self.momentum, eps=self.eps, slope=self.slope,
                         training=self.training, gamma_mode=self.gamma_mode, layout=layout,
-                        comm=self.comm)
+                        comm=self.comm, grad_inplace=self.grad_inplace)
         return z if layout == "NCHW" else z.permute(0, 3, 1, 2)

@@ -219,6 +219,31 @@ def test_autograd_module_matches_oracle():
     assert vec_err(to64(m.weight.grad), dg) < 1e-4 and vec_err(to64(m.bias.grad), db) < 1e-4
 
 
+@pytest.mark.parametrize("share", [True, False], ids=["grad_inplace", "fresh_dx"])
+def test_autograd_gradient_sharing(share):
+    """dL/dx may overwrite dL/dz -- with grad_inplace the gradient reaching
+    the layer's input is the very buffer the layer received; the values match either way."""
+    import paper_1712_02616_b200 as P
+    case = Case(4, 16, 64, seed=14)
+    x, dz, p = inputs(case)
+    seen = {}
+    outs = []
+    for _ in range(2):
+        m = P.InPlaceABN(16, device="cuda", grad_inplace=share)
+        with torch.no_grad():
+            m.weight.copy_(p.gamma)
+            m.bias.copy_(p.beta)
+        xin = x.view(4, 16, 8, 8).cuda().requires_grad_(True)
+        h = xin * 1.0
+        h.register_hook(lambda g: seen.__setitem__("dx", g.data_ptr()))
+        z = m(h)
+        z.register_hook(lambda g: seen.__setitem__("dz", g.data_ptr()))
+        (z * dz.view(4, 16, 8, 8).cuda()).sum().backward()
+        outs.append(xin.grad.clone())
+    assert (seen["dx"] == seen["dz"]) == share
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_channels_last_module():
     import paper_1712_02616_b200 as P
     import oracle
@@ -267,6 +292,26 @@ def test_large_beta_over_gamma(flags):
     compare(case, got, ref, p)
 
 
+@pytest.mark.parametrize("flags", [0, VARIANT_I, STREAM], ids=["II", "I", "streaming"])
+def test_large_beta_over_gamma_bf16(flags):
+    """|beta / gamma| = 20 with bf16 storage.  The stored z is rounded to bf16, so x^
+    recovered from it carries 2^-9 |y| / gamma~ ~ 4 % of error here (reading R9) whatever
+    the reduction; to isolate the BN-dagger cancellation (Q - beta S1)/gamma~ of the
+    default kernels, the expected gradients are the oracle's Alg. 2 from the GPU's own
+    rounded z (in double).  dgamma/dbeta are fp32 outputs: 1e-4."""
+    import oracle
+    from tests.util import vec_err
+    case = Case(8, 16, 784, dtype="bf16", seed=16)
+    x, dz, p = inputs(case)
+    p.beta = (20.0 * p.gamma.abs()).contiguous()
+    got = run_gpu(case, x, dz, p, flags=flags)
+    o = oracle.load()
+    dx, dg, db = o.backward_inplace_I(to64(got["z"]), to64(dz), to64(got["var"]), to64(p.gamma),
+                                      to64(p.beta), eps=case.eps, slope=case.slope)
+    assert chan_err(to64(got["dx"]), dx, 1) < 2e-2
+    assert vec_err(to64(got["dgamma"]), dg) < 1e-4 and vec_err(to64(got["dbeta"]), db) < 1e-4
+
+
 # ------------------------------------------------------------------ streaming kernels at large planes
 @pytest.mark.parametrize("case", [
     Case(3, 5, 64 * 64, dtype="bf16", seed=16),  # bf16, HW >= kThreads * 8: row-cursor apply
@@ -307,40 +352,6 @@ def test_fold_conv(gamma_mode, with_bias, orc):
     assert wo.data_ptr() == wi.data_ptr()
     assert torch.equal(wo.cpu(), torch.from_numpy(w2).float())
     assert torch.equal(bo.cpu(), torch.from_numpy(b2).float())
-
-
-# ------------------------------------------------------------------ one-launch (cooperative) schedule
-ONE = 1 << 10
-COOP_CASES = [
-    Case(8, 40, 196, dtype="f32", seed=20),                    # NCHW aligned
-    Case(8, 40, 196, dtype="bf16", seed=21),                   # NCHW, plane not 16-byte aligned
-    Case(4, 24, 49, dtype="bf16", seed=22),                    # odd plane
-    Case(6, 64, 49, dtype="bf16", layout="NHWC", seed=23),     # NHWC aligned
-    Case(5, 37, 30, dtype="f32", layout="NHWC", seed=24),      # NHWC ragged channels
-    Case(3, 300, 7, dtype="f32", seed=25),                     # many channels, tiny planes
-]
-
-
-@pytest.mark.parametrize("case", COOP_CASES, ids=lambda c: f"{c.layout}_{c.dtype}_{c.N}x{c.C}x{c.HW}")
-def test_coop_parity(case):
-    _check(case, ONE)
-
-
-@pytest.mark.parametrize("case", COOP_CASES[:4], ids=lambda c: f"{c.layout}_{c.dtype}_{c.N}x{c.C}x{c.HW}")
-def test_coop_matches_streaming_bitwise(case):
-    """The one-launch kernel runs the streaming phases with the same partitions."""
-    x, dz, p = inputs(case)
-    a = run_gpu(case, x, dz, p, flags=ONE)
-    b = run_gpu(case, x, dz, p, flags=STREAM)
-    for k in ("z", "mean", "var", "rm", "rv", "dx", "dgamma", "dbeta"):
-        assert torch.equal(a[k], b[k]), k
-
-
-def test_coop_schedule_query():
-    from paper_1712_02616_b200 import _lib as L
-    d = L.desc(32, 512, 196, L.BF16, L.NCHW)  # plane of 392 B: covering-range fused kernels
-    assert L.query_schedule(d, 0)[0] == 1  # the one-launch schedule is opt-in (slower)
-    assert L.query_schedule(d, 0, ONE)[0] == 2 and L.query_schedule(d, 1, ONE)[0] == 2
 
 
 # ------------------------------------------------------------------ streaming at any plane alignment
