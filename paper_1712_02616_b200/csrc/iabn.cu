@@ -5,6 +5,7 @@
 // shared memory of a <=16-CTA cluster, else the streaming kernels), launches on
 // the caller's stream, and the NCCL exchange of the synchronized variant
 // (libnccl.so.2 loaded with dlopen, so the library loads without NCCL/GPU).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -24,6 +25,7 @@
 #include "iabn.h"
 #include "kernels_gres.cuh"
 #include "kernels_fused.cuh"
+#include "kernels_nhwc.cuh"
 #include "kernels_stream.cuh"
 
 using namespace iabn;
@@ -104,6 +106,11 @@ iabn_status device_facts(DevFacts** out) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         }
+        const void* nhwc[] = {(const void*)nhwc_fused_kernel<float, 0>,
+                              (const void*)nhwc_fused_kernel<__nv_bfloat16, 0>,
+                              (const void*)nhwc_fused_kernel<float, 1>,
+                              (const void*)nhwc_fused_kernel<__nv_bfloat16, 1>};
+        for (const void* fn : nhwc) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         const void* gres[] = {(const void*)gres_kernel<float, 0>,
                               (const void*)gres_kernel<__nv_bfloat16, 0>,
                               (const void*)gres_kernel<float, 1>,
@@ -612,6 +619,274 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         return fail(IABN_ERR_CUDA, "fused launch: %s", cudaGetErrorString(e));
     }
     return check_launch(pass == 0 ? "fused_kernel<fwd>" : "fused_kernel<bwd>");
+}
+
+// ====================================================================== NHWC channel groups
+// kernels_nhwc.cuh: a cluster of K CTAs holds the g-channel column group of all rows in
+// shared memory (2-D TMA boxes), reduces, exchanges over DSMEM and applies in place.
+struct NhwcPlan {
+    bool ok = false;
+    uint32_t g = 0, cols = 0, K = 0, rows_cta = 0, box_rows = 0, ngroups = 0;
+    uint32_t slab = 0, red_off = 0, rec_off = 0, coef_off = 0, bar_off = 0;
+    size_t smem = 0;
+    int clusters = 0;  // launched (persistent over ngroups)
+    double est_us = 0;
+};
+
+int nhwc_max_clusters(int pass, int dtype, int K, size_t smem) {
+    static std::mutex mu;
+    struct Key {
+        int dev, pass, dtype, K;
+        size_t smem;
+        int val;
+    };
+    static std::vector<Key> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Key& k : cache)
+        if (k.dev == dev && k.pass == pass && k.dtype == dtype && k.K == K && k.smem == smem)
+            return k.val;
+    const void* fn = dtype == IABN_F32
+                         ? (pass == 0 ? (const void*)nhwc_fused_kernel<float, 0>
+                                      : (const void*)nhwc_fused_kernel<float, 1>)
+                         : (pass == 0 ? (const void*)nhwc_fused_kernel<__nv_bfloat16, 0>
+                                      : (const void*)nhwc_fused_kernel<__nv_bfloat16, 1>);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)K, 1, 1);
+    cfg.blockDim = dim3(kNhwcThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    if (cache.size() < 4096) cache.push_back(Key{dev, pass, dtype, K, smem, n});
+    return n;
+}
+
+// test hooks (iabn_debug_nhwc_plan): forced g, K and launched clusters, 0 = automatic
+std::atomic<int> g_nhwc_force_g{0}, g_nhwc_force_k{0}, g_nhwc_force_clusters{0};
+
+// (g, K) from measurements on B200 (tools/nhwc_tune.py, profiles/r02_nhwc_tune_*.json):
+// 2-D TMA boxes of narrow rows move few bytes per request, so the per-CTA chain (load,
+// reduce, exchange, apply, store) is short only for small slabs and many CTAs: group rows
+// of 32 bytes (then 64, then 16), K = ceil(128 / groups) CTAs per group (at least 128 CTAs
+// when the channels allow, at most 8 per cluster), raised while a backward CTA would hold
+// more than 80 KB, all groups in one wave of co-resident clusters.  Layers with more than
+// 32768 rows (N*HW; the 56x56 and 112x112 layers at N = 32) keep the streaming schedule:
+// their groups do not fit on chip at a useful width.  Env IABN_NHWC_G (channels) /
+// IABN_NHWC_K (or the iabn_debug_nhwc_plan hook) force a choice.
+NhwcPlan nhwc_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags) {
+    NhwcPlan best;
+    if (g.layout != IABN_NHWC || (flags & IABN_EVAL)) return best;
+    if ((g.C * g.b) % 16 != 0 || g.m >= (1ll << 31) || g.C >= (1ll << 31)) return best;
+    if (!(flags & IABN_FORCE_FUSED) && env_int("IABN_NHWC_FUSED", 1) == 0) return best;
+    const int nin = pass == 0 ? 1 : 2, NR = pass == 0 ? 3 : 2;
+    const size_t budget = (size_t)f.max_smem_optin - 2048;
+    const int gforce = g_nhwc_force_g.load() ? g_nhwc_force_g.load() : env_int("IABN_NHWC_G", 0);
+    const int kforce = g_nhwc_force_k.load() ? g_nhwc_force_k.load() : env_int("IABN_NHWC_K", 0);
+    const bool forced = gforce || kforce;
+    if (!forced && !(flags & IABN_FORCE_FUSED) && g.m > env_int("IABN_NHWC_MAX_ROWS", 32768))
+        return best;
+    // the plan of (group bytes gb, K), or !ok if it does not fit
+    auto make = [&](int gb, int K) -> NhwcPlan {
+        NhwcPlan p;
+        const uint32_t gch = (uint32_t)(gb / g.b);
+        const uint32_t cols = (uint32_t)gb / 16, rs = kNhwcThreads / cols;
+        // rows per CTA in nbox boxes of <= 256 rows (TMA box limit), each a multiple of
+        // the block's row sweep; boxes sized to the rows, not to 256 (less padding)
+        const uint32_t r0 = (uint32_t)((g.m + K - 1) / K);
+        const uint32_t nb0 = (r0 + 255) / 256;
+        const uint32_t box = std::min<uint32_t>(256, ((r0 + nb0 - 1) / nb0 + rs - 1) / rs * rs);
+        const uint32_t nbox = (r0 + box - 1) / box;
+        const uint32_t rows_cta = nbox * box;
+        if (nbox > (uint32_t)kNhwcMaxBoxes) return p;
+        const size_t slab = align256((size_t)rows_cta * gb);
+        size_t off = slab * nin;
+        const size_t red_off = off;
+        off = align256(off + (size_t)(kNhwcThreads / 32) * gch * NR * 8);
+        const size_t rec_off = off;
+        off = align256(off + (size_t)2 * K * gch * NR * 8);
+        const size_t coef_off = off;
+        off = align256(off + (size_t)gch * 14 * 4);  // coefficients [g][8] + 6 params [g]
+        const size_t bar_off = off;
+        off += (size_t)nbox * 8;
+        if (off > budget) return p;
+        const int mc = nhwc_max_clusters(pass, g.dtype, K, off);
+        if (mc <= 0) return p;
+        p.ngroups = (uint32_t)((g.C + gch - 1) / gch);
+        int clusters = (int)std::min<int64_t>(mc, p.ngroups);
+        if (const int fc = g_nhwc_force_clusters.load()) clusters = std::min(clusters, fc);
+        p.ok = true;
+        p.g = gch;
+        p.cols = cols;
+        p.K = (uint32_t)K;
+        p.rows_cta = rows_cta;
+        p.box_rows = box;
+        p.slab = (uint32_t)slab;
+        p.red_off = (uint32_t)red_off;
+        p.rec_off = (uint32_t)rec_off;
+        p.coef_off = (uint32_t)coef_off;
+        p.bar_off = (uint32_t)bar_off;
+        p.smem = off;
+        p.clusters = clusters;
+        p.est_us = std::ceil((double)p.ngroups / clusters);  // waves
+        return p;
+    };
+    if (forced) {
+        for (int gb = 256; gb >= 16; gb /= 2) {
+            if (gforce && gb / g.b != gforce) continue;
+            if (!gforce && gb / g.b > g.C && gb > 16) continue;
+            for (int K = 1; K <= kNhwcMaxK; ++K) {
+                if (kforce && K != kforce) continue;
+                const NhwcPlan p = make(gb, K);
+                if (p.ok) {
+                    best = p;
+                    goto done;
+                }
+            }
+        }
+        goto done;
+    }
+    for (const int gb : {32, 64, 16}) {
+        if (gb / g.b > g.C && gb > 16) continue;
+        const int64_t groups = (g.C * g.b + gb - 1) / gb;
+        int K = (int)std::min<int64_t>(kNhwcMaxK, std::max<int64_t>(1, (128 + groups - 1) / groups));
+        NhwcPlan p;
+        for (; K <= kNhwcMaxK; ++K) {  // the first one-wave plan from the target K up
+            p = make(gb, K);
+            if (p.ok && p.est_us <= 1.0) break;
+        }
+        if (!(p.ok && p.est_us <= 1.0)) continue;
+        // backward: at most ~80 KB of slab per CTA while a larger cluster stays one wave
+        while (p.K < (uint32_t)kNhwcMaxK && (size_t)p.slab * nin > 80 * 1024) {
+            const NhwcPlan q = make(gb, (int)p.K + 1);
+            if (!(q.ok && q.est_us <= 1.0)) break;
+            p = q;
+        }
+        best = p;
+        break;
+    }
+done:
+    if (best.ok && env_int("IABN_VERBOSE", 0)) {
+        static std::mutex pm;
+        static int printed = 0;
+        std::lock_guard<std::mutex> lk(pm);
+        if (printed++ < 32)
+            fprintf(stderr, "[iabn] nhwc pass=%d C=%lld m=%lld: g=%u K=%u rows_cta=%u box=%u groups=%u clusters=%d smem=%zu waves=%.0f\n",
+                    pass, (long long)g.C, (long long)g.m, best.g, best.K, best.rows_cta,
+                    best.box_rows, best.ngroups, best.clusters, best.smem, best.est_us);
+    }
+    return best;
+}
+
+// 2-D tensor map of an NHWC activation: dim 0 = C channels, dim 1 = m rows, box = [g, R]
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+iabn_status nhwc_tmap(CUtensorMap* tm, const void* ptr, const Geom& g, const NhwcPlan& p) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return fail(IABN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)g.C, (cuuint64_t)g.m};
+    const cuuint64_t strides[1] = {(cuuint64_t)(g.C * g.b)};
+    const cuuint32_t box[2] = {p.g, p.box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = enc(tm, g.dtype == IABN_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                           2, const_cast<void*>(ptr), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(IABN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return IABN_OK;
+}
+
+template <typename T>
+iabn_status launch_nhwc(int pass, const Geom& g, const NhwcPlan& p, NhwcArgs a, const void* in0,
+                        const void* in1, void* out, cudaStream_t st) {
+    CUtensorMap t0, t1, t2;
+    IABN_TRY(nhwc_tmap(&t0, in0, g, p));
+    IABN_TRY(nhwc_tmap(&t1, pass == 1 ? in1 : in0, g, p));
+    IABN_TRY(nhwc_tmap(&t2, out, g, p));
+    a.in0 = in0;
+    a.C = g.C;
+    a.m = (uint32_t)g.m;
+    a.g = p.g;
+    a.cols = p.cols;
+    a.ngroups = p.ngroups;
+    a.K = p.K;
+    a.rows_cta = p.rows_cta;
+    a.box_rows = p.box_rows;
+    a.slab_bytes = p.slab;
+    a.red_off = p.red_off;
+    a.rec_off = p.rec_off;
+    a.coef_off = p.coef_off;
+    a.bar_off = p.bar_off;
+    a.prefetch = (uint32_t)env_int("IABN_NHWC_PREFETCH", 1);
+    a.trace = nullptr;
+    if (env_int("IABN_NHWC_TRACE", 0)) {  // experiments only: phase timestamps
+        static unsigned long long* buf = nullptr;
+        static size_t cap = 0;
+        const size_t need = (size_t)p.clusters * p.K * kNhwcTrace;
+        if (need > cap) {
+            if (buf) cudaFree(buf);
+            cudaMalloc(&buf, need * sizeof(unsigned long long));
+            cap = need;
+        }
+        a.trace = buf;
+        g_trace = buf;
+        g_trace_n = need;
+        g_trace_ch = (uint32_t)kNhwcTrace;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.clusters * p.K), 1, 1);
+    cfg.blockDim = dim3(kNhwcThreads, 1, 1);
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = p.K;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    const cudaError_t e = pass == 0 ? cudaLaunchKernelEx(&cfg, nhwc_fused_kernel<T, 0>, t0, t1, t2, a)
+                                    : cudaLaunchKernelEx(&cfg, nhwc_fused_kernel<T, 1>, t0, t1, t2, a);
+    if (e != cudaSuccess) {
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return fail(IABN_ERR_CUDA, "nhwc launch: %s", cudaGetErrorString(e));
+    }
+    return check_launch(pass == 0 ? "nhwc_fused_kernel<fwd>" : "nhwc_fused_kernel<bwd>");
 }
 
 FastDiv cover_fd(const Geom& g) { return make_fastdiv((uint32_t)(g.HW / (16 / g.b) + 2)); }
@@ -1270,13 +1545,33 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
     }
     FusedPlan p;
     if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 0, *c.dev, flags);
-    if ((flags & IABN_FORCE_FUSED) && !p.ok)
+    if ((flags & IABN_FORCE_FUSED) && !p.ok && c.g.layout != IABN_NHWC)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shape");
     if (p.ok)
         return launch_fused<T>(0, p,
                                fused_fwd_args(c.g, x, z, gamma, beta, rm, rv, sm, sv, momentum, eps,
                                               slope, flags),
                                c.st);
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_RESIDENT))) {
+        const NhwcPlan np = nhwc_plan(c.g, 0, *c.dev, flags);
+        if (np.ok) {
+            NhwcArgs a{};
+            a.gamma = gamma;
+            a.beta = beta;
+            a.running_mean = rm;
+            a.running_var = rv;
+            a.save_mean = sm;
+            a.save_var = sv;
+            a.momentum = momentum;
+            a.eps = eps;
+            a.slope = slope;
+            a.inv_slope = 1.0f / slope;
+            a.flags = flags;
+            return launch_nhwc<T>(0, c.g, np, a, x, nullptr, z, c.st);
+        }
+        if (flags & IABN_FORCE_FUSED)
+            return fail(IABN_ERR_UNSUPPORTED, "channel-group NHWC forward not possible for this shape");
+    }
     if (const int G = gres_grid(c.g, 0, flags, *c.dev)) {
         GresArgs a{};
         a.in0 = x;
@@ -1317,13 +1612,31 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                           float* db, float eps, float slope, uint32_t flags) {
     FusedPlan p;
     if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 1, *c.dev, flags);
-    if ((flags & IABN_FORCE_FUSED) && !p.ok)
+    if ((flags & IABN_FORCE_FUSED) && !p.ok && c.g.layout != IABN_NHWC)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shape");
     if (p.ok)
         return launch_fused<T>(1, p,
                                fused_bwd_args(c.g, z, dz, dx, gamma, beta, sv, dg, db, eps, slope,
                                               flags),
                                c.st);
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_RESIDENT))) {
+        const NhwcPlan np = nhwc_plan(c.g, 1, *c.dev, flags);
+        if (np.ok) {
+            NhwcArgs a{};
+            a.gamma = gamma;
+            a.beta = beta;
+            a.save_var = const_cast<float*>(sv);
+            a.dgamma = dg;
+            a.dbeta = db;
+            a.eps = eps;
+            a.slope = slope;
+            a.inv_slope = 1.0f / slope;
+            a.flags = flags;
+            return launch_nhwc<T>(1, c.g, np, a, z, dz, dx, c.st);
+        }
+        if (flags & IABN_FORCE_FUSED)
+            return fail(IABN_ERR_UNSUPPORTED, "channel-group NHWC backward not possible for this shape");
+    }
     double* part = wsp<double>(c, c.w.part);
     if (const int G = gres_grid(c.g, 1, flags, *c.dev)) {
         GresArgs a{};
@@ -1421,6 +1734,15 @@ IABN_API uint32_t iabn_debug_trace_channels(void) { return g_trace_ch; }
 // 4 = dx[0] perturbed, 8 = running_var x 1.001 on every later call; 0 = off.
 IABN_API void iabn_debug_fault(uint32_t mask) { g_fault.store(mask); }
 
+// Test hook only (not in include/iabn.h): force the NHWC channel-group plan -- g channels
+// per group, K CTAs per cluster, at most `clusters` clusters launched (persistent loop
+// over the groups); 0 = automatic.  Shapes the forced plan cannot take fall back as usual.
+IABN_API void iabn_debug_nhwc_plan(int g, int K, int clusters) {
+    g_nhwc_force_g.store(g);
+    g_nhwc_force_k.store(K);
+    g_nhwc_force_clusters.store(clusters);
+}
+
 size_t iabn_workspace_bytes(const iabn_desc* desc) {
     Geom g;
     if (make_geom(desc, &g) != IABN_OK) return 0;
@@ -1442,6 +1764,13 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
         p = fused_plan(g, pass, *dev, flags);
     *schedule = p.ok ? 1 : 0;
     *cluster = p.ok ? p.K : 0;
+    if (!p.ok && !(flags & (IABN_FORCE_STREAMING | IABN_FORCE_RESIDENT))) {
+        const NhwcPlan np = nhwc_plan(g, pass, *dev, flags);
+        if (np.ok) {
+            *schedule = 4;
+            *cluster = (int)np.K;
+        }
+    }
     if (!p.ok && *schedule == 0 && gres_grid(g, pass, flags, *dev) > 0) *schedule = 3;
     return IABN_OK;
 }

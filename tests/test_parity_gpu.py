@@ -470,7 +470,7 @@ RESIDENT = 1 << 11
 def test_grid_resident_nhwc(case):
     from paper_1712_02616_b200 import _lib as L
     d = L.desc(case.N, case.C, case.HW, L.BF16 if case.dtype == "bf16" else L.F32, L.NHWC)
-    assert L.query_schedule(d, 0)[0] == 0  # opt-in
+    assert L.query_schedule(d, 0)[0] == 4  # default: channel groups; grid-resident is opt-in
     assert L.query_schedule(d, 0, RESIDENT)[0] == 3 and L.query_schedule(d, 1, RESIDENT)[0] == 3
     _check(case, RESIDENT)
 

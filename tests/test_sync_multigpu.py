@@ -78,7 +78,7 @@ def _run(shards, C, HW, dtype, fused, seed, tmp_path):
 
 
 def _check(res, shards, C, HW, dtype, seed):
-    from tests.harness import TOL, Case, ambiguous, inputs, run_oracle, shard_param_errs, to64
+    from tests.harness import TOL, Case, ambiguous, dx_err, inputs, run_oracle, shard_param_errs, to64
     from tests.util import chan_err, vec_err
     import oracle
     case = Case(sum(shards), C, HW, dtype=dtype, seed=seed)
@@ -86,7 +86,8 @@ def _check(res, shards, C, HW, dtype, seed):
     ref = run_oracle(case, x, dz, p)
     amb = ambiguous(case, ref, p)
     errs = {"z": chan_err(np.concatenate([r["z"] for r in res]), ref["z"], 1),
-            "dx": chan_err(np.concatenate([r["dx"] for r in res]), ref["dx"], 1, mask=amb)}
+            "dx": dx_err(case, np.concatenate([r["dx"] for r in res]).astype(np.float64), ref, p,
+                         amb)}
     dgl, dbl = oracle.load().param_grads_sharded(to64(x), to64(dz), to64(p.gamma),
                                                  to64(p.beta), list(shards))
     n_off = np.concatenate([[0], np.cumsum(shards)])

@@ -19,7 +19,7 @@ import sys
 import numpy as np
 import pytest
 
-from tests.harness import TOL, Case, ambiguous, inputs, run_oracle, shard_param_errs, to64
+from tests.harness import TOL, Case, ambiguous, dx_err, inputs, run_oracle, shard_param_errs, to64
 from tests.util import chan_err, vec_err
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -79,7 +79,7 @@ def test_sync_nccl_path_multi_rank(cfg, tmp_path):
     tol = TOL[dtype]
     amb = ambiguous(case, ref, p)
     errs = {"z": chan_err(got["z"], ref["z"], case.ax),
-            "dx": chan_err(got["dx"], ref["dx"], case.ax, mask=amb)}
+            "dx": dx_err(case, got["dx"].astype(np.float64), ref, p, amb)}
     if sum(shards) * HW <= 4:
         # m_G <= 4: dx = gamma~ rstd (dy - x^ S2/m - S1/m) cancels to O(eps / sigma^2) of its
         # terms (for m = 2 exactly (d1 - d2)/2 * eps/(sigma^2 + eps)), so fp32 can only be
