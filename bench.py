@@ -685,7 +685,13 @@ def run_rank(args, wl, pl, make_comm, emulated: bool):
     # ---- synchronized variant on one GPU: the fused-collective kernels over G virtual ranks
     sync_emu = None
     G = args.sync_emulated
-    if world == 1 and G > 1 and wl["N"] % G == 0 and wl["layout"] == "NCHW":
+    profiled = any(k in os.environ for k in ("NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                                             "NV_COMPUTE_PROFILER_PERFWORKS_DIR",
+                                             "CUDA_INJECTION64_PATH"))
+    if profiled and G > 1 and not os.environ.get("IABN_EMU_NONCOOP"):
+        # Nsight Compute cannot launch the emulation's cooperative cluster kernels
+        sync_emu = {"skipped": "profiler attached (cooperative cluster launch unsupported)"}
+    elif world == 1 and G > 1 and wl["N"] % G == 0 and wl["layout"] == "NCHW":
         for _ in range(3):
             z, _, sv = P.forward_sync_emulated(x, G, g, bt, rm, rv)
             P.backward_sync_emulated(z, dz, G, g, bt, sv)

@@ -589,7 +589,10 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
     }
-    if (a.vranks > 1) {
+    // IABN_EMU_NONCOOP=1 (experiments only): a plain launch of the emulation -- Nsight
+    // Compute cannot launch a cooperative cluster kernel ("LaunchFailed"); under its
+    // kernel replay the grid (<= the co-resident clusters) runs alone, so it is resident
+    if (a.vranks > 1 && !env_int("IABN_EMU_NONCOOP", 0)) {
         at[na].id = cudaLaunchAttributeCooperative;
         at[na].val.cooperative = 1;
         ++na;

@@ -95,6 +95,29 @@ __global__ void tma_stream(const uint4* __restrict__ in, uint4* __restrict__ out
     if (acc == 0xdeadbeef) *sink = acc;
 }
 
+// plain LDG/STG, 2 reads : 1 write (the fused backward's mix: z, dz in, dx out)
+template <int UNROLL>
+__global__ void ldg_2r1w(const uint4* __restrict__ in, const uint4* __restrict__ in2,
+                         uint4* __restrict__ out, size_t nvec) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t base = (size_t)blockIdx.x * blockDim.x + threadIdx.x; base < nvec; base += stride * UNROLL) {
+        uint4 r[UNROLL], q[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            size_t i = base + u * stride;
+            if (i < nvec) {
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w) : "l"(in + i));
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(q[u].x), "=r"(q[u].y), "=r"(q[u].z), "=r"(q[u].w) : "l"(in2 + i));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+            size_t i = base + u * stride;
+            if (i < nvec) out[i] = make_uint4(r[u].x ^ q[u].x, r[u].y ^ q[u].y, r[u].z ^ q[u].z, r[u].w ^ q[u].w);
+        }
+    }
+}
+
 // plain LDG/STG: read-only reduce (mode 0) or copy (mode 1), UNROLL vectors in flight
 template <int UNROLL>
 __global__ void ldg_stream(const uint4* __restrict__ in, uint4* __restrict__ out, size_t nvec,
@@ -120,7 +143,8 @@ __global__ void ldg_stream(const uint4* __restrict__ in, uint4* __restrict__ out
     if (acc == 0xdeadbeef) *sink = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
+    const bool quick = argc > 1;  // any argument: the LDG variants only
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     const size_t bytes = (size_t)1644 << 20;  // ~1.64 GB, the cfg4 bf16 tensor
@@ -130,7 +154,10 @@ int main() {
     CK(cudaMalloc(&in, bytes));
     CK(cudaMalloc(&out, bytes));
     CK(cudaMalloc(&sink, 4));
+    uint4* in2;
+    CK(cudaMalloc(&in2, bytes));
     CK(cudaMemset(in, 1, bytes));
+    CK(cudaMemset(in2, 2, bytes));
     CK(cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -162,6 +189,14 @@ int main() {
             if (u == 16) timeit([&] { ldg_stream<16><<<grid, 256>>>(in, out, nvec, 1, sink); }, 2.0 * bytes, name);
         }
     }
+    for (int bps : {2, 4, 8}) {
+        const int grid = sms * bps;
+        snprintf(name, sizeof name, "ldg 2r1w  unroll=4 ctas/sm=%d", bps);
+        timeit([&] { ldg_2r1w<4><<<grid, 256>>>(in, in2, out, nvec); }, 3.0 * bytes, name);
+        snprintf(name, sizeof name, "ldg 2r1w  unroll=8 ctas/sm=%d", bps);
+        timeit([&] { ldg_2r1w<8><<<grid, 256>>>(in, in2, out, nvec); }, 3.0 * bytes, name);
+    }
+    if (quick) return 0;
     for (int mode : {0, 1, 2}) {
         for (int ckb : {4, 8, 16, 32}) {
             for (int bps : {1, 2, 4}) {
