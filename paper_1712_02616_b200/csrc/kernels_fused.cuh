@@ -96,7 +96,11 @@ struct FusedArgs {
                      // into `trace`
     unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
     uint32_t trace_ch;          // channels per CTA recorded
+    // dynamic channel scheduling (one rank): [0] ticket counter, [1] clusters finished;
+    // zero at launch, reset by the last cluster; nullptr = static (cluster q: q, q + Q, ..)
+    unsigned int* dyn;
 };
+constexpr int kChanRing = 16;  // channel numbers in flight per CTA (dynamic scheduling)
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -306,6 +310,8 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     __shared__ Terms lterm[kSlots];                                // sync: channel terms
     __shared__ double red[2][2][kReduceWarps];
     __shared__ ApplyCoef cs[2];
+    __shared__ uint32_t chan_ring[kChanRing];               // channel of slot t (dynamic)
+    __shared__ __align__(8) uint64_t chanbar[kChanRing];    // chan_ring[t % R] has landed
 
     const uint32_t K = cluster_nctarank(), r = cluster_ctarank();
     const uint32_t cid = blockIdx.x / K;       // cluster
@@ -345,12 +351,27 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             mbar_init(&ready[i], 1);
             mbar_init(&freed[i], apply_warps);
         }
+        for (int i = 0; i < kChanRing; ++i) mbar_init(&chanbar[i], 1);
         fence_mbar_init();
     }
     // every CTA's barriers are initialised before any peer may arrive on them
     cluster_arrive_release();
     cluster_wait_acquire();
     pdl_wait();  // the prologue above overlaps the previous kernel's tail
+
+    // Channel of slot t.  Static: q + t Q.  Dynamic (a.dyn, one rank): cluster q starts
+    // with channel q, then takes tickets Q + atomicAdd(dyn[0]) -- clusters that finish
+    // early take more channels, so the grid's tail shrinks to about one channel (static
+    // striding left CTAs idle for up to 8 % of the forward, profiles/r01_trace_phases_k8).
+    // CTA 0's producer draws the ticket and stores it into every CTA's chan_ring with
+    // st.async (complete_tx on chanbar); every role waits on chanbar before reading it.
+    // C = no more channels.
+    const bool dynamic = MINB == 2 && a.dyn != nullptr;  // compiled out of the small-slab variant
+    auto chan_of = [&](uint32_t t) -> uint32_t {
+        if (!dynamic) return t < nT ? q + t * Q : C;
+        mbar_wait(&chanbar[t % kChanRing], (t / kChanRing) & 1u);
+        return *(volatile uint32_t*)&chan_ring[t % kChanRing];
+    };
 
     if (warp == kProducerWarp) {
         // ================================================ producer: slab t into buffer t % nbuf,
@@ -368,9 +389,40 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             const uint32_t nl = wide ? 32u : 1u;  // lanes issuing copies
             const T* src[2] = {(const T*)a.in0 + voff, (const T*)a.in1 + voff};
             const uint32_t hw = (uint32_t)a.HW;
-            for (uint32_t t = 0; t < nT; ++t) {
+            uint32_t published = 0;  // dynamic: slots whose channel CTA 0 has stored
+            bool exhausted = false;
+            auto publish = [&](uint32_t u) {  // CTA 0, lane 0
+                uint32_t c = C;
+                if (!exhausted) {
+                    c = u == 0 ? q : Q + atomicAdd(&a.dyn[0], 1u);
+                    if (c >= C) {
+                        c = C;
+                        exhausted = true;
+                    }
+                }
+                const uint32_t i = u % kChanRing;
+                for (uint32_t j = 0; j < K; ++j)
+                    asm volatile(
+                        "st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                            mapa(&chan_ring[i], j)),
+                        "r"(c), "r"(mapa(&chanbar[i], j))
+                        : "memory");
+            };
+            for (uint32_t t = 0;; ++t) {
+                uint32_t cu;
+                if (dynamic) {
+                    if (lane == 0) {
+                        if (r == 0)  // one slot ahead: the peers' producers need not wait
+                            while (published <= t + 1) publish(published++);
+                        mbar_arrive_expect_tx(&chanbar[t % kChanRing], 4u);
+                    }
+                    cu = chan_of(t);
+                } else {
+                    cu = t < nT ? q + t * Q : C;
+                }
+                if (cu >= C) break;
                 const uint32_t b = t % nbuf;
-                const int64_t c = q + t * Q;
+                const int64_t c = cu;
                 uint4* buf = smem + b * bufv;
                 // one decision per slice (not per copy: the producer lane issues one bulk
                 // copy per plane, ~100 per slice on 14x14 layers)
@@ -571,8 +623,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             }
         };
         if (a.nranks <= 1) {
-            for (uint32_t s = 0; s < nT; ++s) {
-                const int64_t cp = q + s * Q;
+            for (uint32_t s = 0;; ++s) {
+                const uint32_t cs_ = chan_of(s);
+                if (cs_ >= C) break;
+                const int64_t cp = cs_;
                 const uint32_t rs = s % kSlots;
                 if (s >= 2) mbar_wait(&freed[s & 1u], (s / 2 - 1) & 1u);
                 const Terms t = terms(cp);
@@ -681,11 +735,11 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     // ==================================================== reduce (slice t): channel sums over
     // the resident slice; the CTA record is pushed into all K peers (DSMEM).  Threads
     // tid < RT of a group with named barrier gb; warp tid / 32 == 0 folds and pushes.
-    auto reduce_slice = [&](const uint32_t t, const uint32_t tid, const uint32_t RT,
-                            const uint32_t gb) {
+    auto reduce_slice = [&](const uint32_t t, const uint32_t ct, const uint32_t tid,
+                            const uint32_t RT, const uint32_t gb) {
         const uint32_t gw = tid >> 5;
         {
-            const int64_t c = q + t * Q;
+            const int64_t c = ct;
             const uint32_t b = t % nbuf, par = (t / nbuf) & 1u;
             const uint32_t xs = smem_u32 + (uint32_t)(b * bufv * 16);  // x (fwd) or z (bwd)
             const uint32_t ds = xs + a.cap * 16u;                      // dz (bwd)
@@ -945,13 +999,13 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     // ==================================================== apply (slice s): outputs from the
     // resident slice once the channel's coefficients are in (the reduce has read it by then).
     // Threads at < AT of a group with named barrier gb; warp 0 of the group polls.
-    auto apply_slice = [&](const uint32_t s, const uint32_t at, const uint32_t AT,
-                           const uint32_t gb) {
+    auto apply_slice = [&](const uint32_t s, const uint32_t cs_, const uint32_t at,
+                           const uint32_t AT, const uint32_t gb) {
         const uint32_t hw = (uint32_t)a.HW;
         const float2 sl2 = make_float2(a.slope, a.slope);
         T* out = (T*)a.out + voff;
         const int64_t chw = a.C * a.HW;
-        const int64_t cp = q + s * Q;
+        const int64_t cp = cs_;
         const uint32_t b = s % nbuf, slot = s & 1u;
         group_wait(&ready[slot], (s / 2) & 1u, at < 32, gb, AT);
         if (at == 0) IABN_TRACE(a, s, 6);
@@ -1153,15 +1207,29 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     if (warp == kProducerWarp || warp == kExchangeWarp) {
         // above
     } else if (warp >= (uint32_t)kReduceWarp0 && warp < (uint32_t)(kReduceWarp0 + kReduceWarps)) {
-        for (uint32_t t = 0; t < nT; ++t)
-            reduce_slice(t, threadIdx.x - kReduceWarp0 * 32, kReduceWarps * 32, 1);
+        for (uint32_t t = 0;; ++t) {
+            const uint32_t ct = chan_of(t);
+            if (ct >= C) break;
+            reduce_slice(t, ct, threadIdx.x - kReduceWarp0 * 32, kReduceWarps * 32, 1);
+        }
     } else {
-        for (uint32_t s = 0; s < nT; ++s)
-            apply_slice(s, threadIdx.x - kApplyWarp0 * 32, kApplyWarps * 32, 2);
+        for (uint32_t s = 0;; ++s) {
+            const uint32_t cs_ = chan_of(s);
+            if (cs_ >= C) break;
+            apply_slice(s, cs_, threadIdx.x - kApplyWarp0 * 32, kApplyWarps * 32, 2);
+        }
     }
     // peers may still push records / arrive on this CTA's barriers until they finish
     cluster_arrive_release();
     cluster_wait_acquire();
+    if (dynamic && r == 0 && threadIdx.x == 0) {
+        // the last cluster (every ticket is drawn by then) re-arms the counters
+        __threadfence();
+        if (atomicAdd(&a.dyn[1], 1u) == gridDim.x / K - 1) {
+            atomicExch(&a.dyn[0], 0u);
+            atomicExch(&a.dyn[1], 0u);
+        }
+    }
     if (a.nranks > 1 && threadIdx.x == 0) {
         // the grid's last CTA advances the call number for the next call on this stream
         __threadfence();
