@@ -26,6 +26,7 @@
 #include "kernels_gres.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_nhwc.cuh"
+#include "kernels_small.cuh"
 #include "kernels_stream.cuh"
 
 using namespace iabn;
@@ -835,6 +836,53 @@ done:
     return best;
 }
 
+// ====================================================================== small NCHW layers
+// kernels_small.cuh: a channel's covering 16-byte slots held in the registers of a team of
+// 32*tw threads (<= kSmallR slots per thread), one launch per pass.
+struct SmallPlan {
+    bool ok = false;
+    uint32_t W = 0, tw = 0;
+    unsigned grid = 0;
+};
+std::atomic<int> g_small_force{0};  // test hook: 1 on when possible, -1 off, 0 automatic
+
+SmallPlan small_plan(const Geom& g, uint32_t flags) {
+    SmallPlan p;
+    if (g.layout != IABN_NCHW || (flags & IABN_EVAL)) return p;
+    const int f = g_small_force.load();
+    if (f < 0 || (!f && !env_int("IABN_SMALL", 1))) return p;
+    if ((g.E * g.b) % 16 != 0 || g.C >= (1ll << 31)) return p;  // the last plane's covering range
+    // measured (tools/small_tune.py, profiles/r02_small_tune_*.log): faster than the
+    // channel-resident kernels up to 16 KB per channel (bf16 14x14 and every 7x7 layer at
+    // N = 32: -25..-42 % per pass); at 25 KB (fp32 14x14) equal or slower
+    if (!f && g.m * g.b > (int64_t)env_int("IABN_SMALL_MAX_KB", 16) * 1024) return p;
+    const int64_t W = (g.HW * g.b + 30) / 16;  // >= the slots covering any plane
+    for (uint32_t tw : {1u, 2u, 4u, 8u}) {
+        if (g.N * W <= (int64_t)32 * tw * kSmallR) {
+            p.ok = true;
+            p.W = (uint32_t)W;
+            p.tw = tw;
+            const int64_t per = (kSmallThreads / 32) / tw;  // channels per CTA
+            p.grid = (unsigned)((g.C + per - 1) / per);
+            return p;
+        }
+    }
+    return p;
+}
+
+template <typename T>
+iabn_status launch_small(int pass, const Geom& g, const SmallPlan& p, SmallArgs a, cudaStream_t st) {
+    a.C = g.C;
+    a.HW = g.HW;
+    a.N = (uint32_t)g.N;
+    a.W = p.W;
+    a.fd_w = fd32(p.W);
+    a.tw = p.tw;
+    if (pass == 0) launch_pdl(small_kernel<T, 0>, p.grid, kSmallThreads, 0, st, a);
+    else launch_pdl(small_kernel<T, 1>, p.grid, kSmallThreads, 0, st, a);
+    return check_launch(pass == 0 ? "small_kernel<fwd>" : "small_kernel<bwd>");
+}
+
 // 2-D tensor map of an NHWC activation: dim 0 = C channels, dim 1 = m rows, box = [g, R]
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1590,6 +1638,26 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         IABN_TRY(check_launch("eval_coef kernel"));
         return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
     }
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
+        const SmallPlan sp = small_plan(c.g, flags);
+        if (sp.ok) {
+            SmallArgs a{};
+            a.in0 = x;
+            a.out = z;
+            a.gamma = gamma;
+            a.beta = beta;
+            a.running_mean = rm;
+            a.running_var = rv;
+            a.save_mean = sm;
+            a.save_var = sv;
+            a.momentum = momentum;
+            a.eps = eps;
+            a.slope = slope;
+            a.inv_slope = 1.0f / slope;
+            a.flags = flags;
+            return launch_small<T>(0, c.g, sp, a, c.st);
+        }
+    }
     FusedPlan p;
     if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 0, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok && c.g.layout != IABN_NHWC)
@@ -1657,6 +1725,25 @@ template <typename T>
 iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                           const float* gamma, const float* beta, const float* sv, float* dg,
                           float* db, float eps, float slope, uint32_t flags) {
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
+        const SmallPlan sp = small_plan(c.g, flags);
+        if (sp.ok) {
+            SmallArgs a{};
+            a.in0 = z;
+            a.in1 = dz;
+            a.out = dx;
+            a.gamma = gamma;
+            a.beta = beta;
+            a.save_var = const_cast<float*>(sv);
+            a.dgamma = dg;
+            a.dbeta = db;
+            a.eps = eps;
+            a.slope = slope;
+            a.inv_slope = 1.0f / slope;
+            a.flags = flags;
+            return launch_small<T>(1, c.g, sp, a, c.st);
+        }
+    }
     FusedPlan p;
     if (!(flags & IABN_FORCE_STREAMING)) p = fused_plan(c.g, 1, *c.dev, flags);
     if ((flags & IABN_FORCE_FUSED) && !p.ok && c.g.layout != IABN_NHWC)
@@ -1721,8 +1808,8 @@ __global__ void fault_scale_kernel(float* v, int64_t n) {
 }
 __global__ void fault_act_kernel(void* a, int dtype) {
     if (dtype == IABN_F32) {
-        float* f = (float*)a;
-        f[0] = f[0] * 1.001f + 1e-3f;
+        float* f = (float*)a;  // well above the fp32 tolerance plus the R16 allowances
+        f[0] = f[0] * 1.01f + 1e-2f;
     } else {
         __nv_bfloat16* h = (__nv_bfloat16*)a;  // bf16 tolerance is 2e-2: a larger step
         const float v = __bfloat162float(h[0]);
@@ -1784,6 +1871,10 @@ IABN_API void iabn_debug_fault(uint32_t mask) { g_fault.store(mask); }
 // Test hook only (not in include/iabn.h): force the NHWC channel-group plan -- g channels
 // per group, K CTAs per cluster, at most `clusters` clusters launched (persistent loop
 // over the groups); 0 = automatic.  Shapes the forced plan cannot take fall back as usual.
+// Test hook only (not in include/iabn.h): the register-resident small-layer schedule --
+// 1 = whenever the shape allows it (ignoring the size threshold), -1 = never, 0 = automatic.
+IABN_API void iabn_debug_small(int on) { g_small_force.store(on); }
+
 // Test hook only (not in include/iabn.h): 1 if the last channel-resident launch drew its
 // channels dynamically (ticket counter), 0 if it used the static order.
 IABN_API int iabn_debug_last_dynamic(void) { return g_last_dyn.load(); }
@@ -1810,6 +1901,14 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     if (pass != 0 && pass != 1) return fail(IABN_ERR_INVALID_ARG, "pass must be 0 or 1");
     DevFacts* dev;
     IABN_TRY(device_facts(&dev));
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
+        const SmallPlan sp = small_plan(g, flags);
+        if (sp.ok) {
+            *schedule = 5;
+            *cluster = 0;
+            return IABN_OK;
+        }
+    }
     FusedPlan p;
     if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL)))
         p = fused_plan(g, pass, *dev, flags);

@@ -35,11 +35,13 @@ def test_cfg1_tiny(seed, flags):
     _check(Case(2, 8, 16, seed=seed), flags)
 
 
-def test_cfg1_tiny_is_fused_by_default():
+def test_cfg1_tiny_is_on_chip_by_default():
+    """cfg1 takes a one-launch on-chip schedule (register-resident small layers, or the
+    channel-resident kernels)."""
     from paper_1712_02616_b200 import _lib as L
     d = L.desc(2, 8, 16, L.F32, L.NCHW)
-    assert L.query_schedule(d, 0)[0] == 1
-    assert L.query_schedule(d, 1)[0] == 1
+    assert L.query_schedule(d, 0)[0] in (1, 5)
+    assert L.query_schedule(d, 1)[0] in (1, 5)
 
 
 # ------------------------------------------------------------------ ragged / edge shapes

@@ -136,7 +136,7 @@ def test_sync_fused_matches_single_rank_fused():
     from tests.harness import run_gpu
     case = Case(8, 48, 196, dtype="f32", seed=35)
     x, dz, p = inputs(case)
-    eager = run_gpu(case, x, dz, p, dx_inplace=False)
+    eager = run_gpu(case, x, dz, p, dx_inplace=False, flags=1 << 9)  # channel-resident
     out = _run(case, 1, x, dz, p)
     assert torch.equal(out["z"].cpu(), eager["z"])
     assert torch.equal(out["dx"].cpu(), eager["dx"])
