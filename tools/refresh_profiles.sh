@@ -1,4 +1,4 @@
-# copy the outputs of tools/gpu_final.sh (gpurun_out/fin_*) into profiles/ (round $1, default r01)
+# copy the outputs of tools/experiments/gpu_final.sh (gpurun_out/fin_*) into profiles/ (round $1, default r01)
 set -e
 R=${1:-r01}; G=gpurun_out; P=profiles
 grep '^{' $G/fin_bench.log | tail -1 > $P/${R}_bench.jsonl
