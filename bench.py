@@ -411,7 +411,9 @@ def preflight_fused(args, pl) -> tuple[bool, str]:
     """Every rank runs preflight_child in a subprocess (its own NCCL group on another
     port); the fused path is used only if every child exits 0."""
     import subprocess
-    env = dict(os.environ)
+    # a fresh rendezvous of the children on another port; torchrun's agent store (which the
+    # parent's process group uses when TORCHELASTIC_USE_AGENT_STORE is set) must not be reused
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC")}
     env["MASTER_PORT"] = str(int(os.environ.get("MASTER_PORT", "29500")) + 17)
     cmd = [sys.executable, os.path.abspath(__file__), "--preflight-fused", "--config", args.config]
     try:
