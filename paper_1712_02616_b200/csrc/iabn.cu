@@ -841,10 +841,11 @@ done:
 // 32*tw threads (<= kSmallR slots per thread), one launch per pass.
 struct SmallPlan {
     bool ok = false;
-    uint32_t W = 0, tw = 0;
+    uint32_t W = 0, tw = 0, R = 0;
     unsigned grid = 0;
 };
 std::atomic<int> g_small_force{0};  // test hook: 1 on when possible, -1 off, 0 automatic
+std::atomic<int> g_small_force_r{0};  // test hook: slots per thread (4 or 8), 0 automatic
 
 SmallPlan small_plan(const Geom& g, uint32_t flags) {
     SmallPlan p;
@@ -857,16 +858,28 @@ SmallPlan small_plan(const Geom& g, uint32_t flags) {
     // N = 32: -25..-42 % per pass); at 25 KB (fp32 14x14) equal or slower
     if (!f && g.m * g.b > (int64_t)env_int("IABN_SMALL_MAX_KB", 16) * 1024) return p;
     const int64_t W = (g.HW * g.b + 30) / 16;  // >= the slots covering any plane
-    for (uint32_t tw : {1u, 2u, 4u, 8u}) {
-        if (g.N * W <= (int64_t)32 * tw * kSmallR) {
-            p.ok = true;
-            p.W = (uint32_t)W;
-            p.tw = tw;
-            const int64_t per = (kSmallThreads / 32) / tw;  // channels per CTA
-            p.grid = (unsigned)((g.C + per - 1) / per);
-            return p;
+    auto fit = [&](uint32_t R, SmallPlan& q) {
+        for (uint32_t tw : {1u, 2u, 4u, 8u}) {
+            if (g.N * W <= (int64_t)32 * tw * R) {
+                q.ok = true;
+                q.W = (uint32_t)W;
+                q.tw = tw;
+                q.R = R;
+                const int64_t per = (kSmallThreads / 32) / tw;  // channels per CTA
+                q.grid = (unsigned)((g.C + per - 1) / per);
+                return true;
+            }
         }
-    }
+        return false;
+    };
+    // R = 4 (thinner warps, more of them in flight) wherever a team of <= 8 warps holds the
+    // channel: measured faster on every 7x7 and bf16 14x14 layer but one (bf16 512x14^2
+    // backward +6 %), e.g. bf16 128x14^2 5.9 / 7.4 -> 4.2 / 4.8 us, 2688x7^2 13.7 / 19.1 ->
+    // 11.9 / 14.3 us; else R = 8.  Forced R (test hook / IABN_SMALL_R): preferred when it fits.
+    const int fr = g_small_force_r.load() ? g_small_force_r.load() : env_int("IABN_SMALL_R", 0);
+    if (fr == 8 && fit(8, p)) return p;
+    if (fit(4, p)) return p;
+    fit(8, p);
     return p;
 }
 
@@ -878,8 +891,13 @@ iabn_status launch_small(int pass, const Geom& g, const SmallPlan& p, SmallArgs 
     a.W = p.W;
     a.fd_w = fd32(p.W);
     a.tw = p.tw;
-    if (pass == 0) launch_pdl(small_kernel<T, 0>, p.grid, kSmallThreads, 0, st, a);
-    else launch_pdl(small_kernel<T, 1>, p.grid, kSmallThreads, 0, st, a);
+    if (p.R == 4) {
+        if (pass == 0) launch_pdl(small_kernel<T, 0, 4>, p.grid, kSmallThreads, 0, st, a);
+        else launch_pdl(small_kernel<T, 1, 4>, p.grid, kSmallThreads, 0, st, a);
+    } else {
+        if (pass == 0) launch_pdl(small_kernel<T, 0, 8>, p.grid, kSmallThreads, 0, st, a);
+        else launch_pdl(small_kernel<T, 1, 8>, p.grid, kSmallThreads, 0, st, a);
+    }
     return check_launch(pass == 0 ? "small_kernel<fwd>" : "small_kernel<bwd>");
 }
 
@@ -1874,6 +1892,8 @@ IABN_API void iabn_debug_fault(uint32_t mask) { g_fault.store(mask); }
 // Test hook only (not in include/iabn.h): the register-resident small-layer schedule --
 // 1 = whenever the shape allows it (ignoring the size threshold), -1 = never, 0 = automatic.
 IABN_API void iabn_debug_small(int on) { g_small_force.store(on); }
+// ... and its slots per thread (4 or 8; 0 = automatic)
+IABN_API void iabn_debug_small_r(int r) { g_small_force_r.store(r); }
 
 // Test hook only (not in include/iabn.h): 1 if the last channel-resident launch drew its
 // channels dynamically (ticket counter), 0 if it used the static order.

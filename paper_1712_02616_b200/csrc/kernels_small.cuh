@@ -27,7 +27,7 @@
 namespace iabn {
 
 constexpr int kSmallThreads = 256;
-constexpr int kSmallR = 8;  // 16-byte slots per thread and input
+constexpr int kSmallR = 8;  // most 16-byte slots per thread and input (R = 4 or 8)
 
 struct SmallArgs {
     const void* in0;  // forward: x; backward: z
@@ -65,8 +65,9 @@ __device__ __forceinline__ uint4 ldg_coherent(const void* p) {
     return r;
 }
 
-template <typename T, int PASS>
-__global__ void __launch_bounds__(kSmallThreads, PASS == 0 ? 3 : 2) small_kernel(const SmallArgs a) {
+template <typename T, int PASS, int R>
+__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? 4 : 3) : (PASS == 0 ? 3 : 2))
+    small_kernel(const SmallArgs a) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
     constexpr uint32_t B = sizeof(T);
@@ -103,9 +104,9 @@ __global__ void __launch_bounds__(kSmallThreads, PASS == 0 ? 3 : 2) small_kernel
         return sl;
     };
     // ---- load the channel's covering slots into registers (all loads in flight)
-    uint4 xr[kSmallR], dr[kSmallR];
+    uint4 xr[R], dr[R];
 #pragma unroll
-    for (int k = 0; k < kSmallR; ++k) {
+    for (int k = 0; k < R; ++k) {
         const Slot sl = slot(k);
         if (sl.ok) {
             xr[k] = ldg_coherent(in0 + sl.off);
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kSmallThreads, PASS == 0 ? 3 : 2) small_kernel
     // ---- per-thread sums
     float s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-    for (int k = 0; k < kSmallR; ++k) {
+    for (int k = 0; k < R; ++k) {
         const Slot sl = slot(k);
         if (!sl.ok) continue;
         const bool inner = sl.si * 16u >= sl.h && sl.si * 16u + 16u <= sl.h + hwb;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(kSmallThreads, PASS == 0 ? 3 : 2) small_kernel
                 c4 = PASS == 1 ? co[4] : 0.f;
     char* out = static_cast<char*>(a.out);
 #pragma unroll
-    for (int k = 0; k < kSmallR; ++k) {
+    for (int k = 0; k < R; ++k) {
         const Slot sl = slot(k);
         if (!sl.ok) continue;
         const bool inner = sl.si * 16u >= sl.h && sl.si * 16u + 16u <= sl.h + hwb;

@@ -18,15 +18,18 @@ pytestmark = pytest.mark.gpu
 VARIANT_I = 1 << 5
 
 
-@pytest.fixture
-def small():
+@pytest.fixture(params=[4, 8], ids=["R4", "R8"])
+def small(request):
     from paper_1712_02616_b200 import _lib as L
-    f = L.lib.iabn_debug_small
-    f.argtypes = [ctypes.c_int]
-    f.restype = None
+    f, fr = L.lib.iabn_debug_small, L.lib.iabn_debug_small_r
+    for h in (f, fr):
+        h.argtypes = [ctypes.c_int]
+        h.restype = None
     f(1)
+    fr(request.param)
     yield
     f(0)
+    fr(0)
 
 
 CASES = [

@@ -18,6 +18,9 @@ from paper_1712_02616_b200 import _lib as L  # noqa: E402
 hook = L.lib.iabn_debug_small
 hook.argtypes = [ctypes.c_int]
 hook.restype = None
+hook_r = L.lib.iabn_debug_small_r
+hook_r.argtypes = [ctypes.c_int]
+hook_r.restype = None
 ap = argparse.ArgumentParser()
 ap.add_argument("--dtype", default="bf16")
 ap.add_argument("--shapes", default="512x196,1024x196,1024x49,2048x49,128x196,128x49,512x784")
@@ -72,9 +75,13 @@ for sh in args.shapes.split(","):
     hook(-1)
     rows["channel-resident"] = [time_pass(xs, dzs, g, bt, p) for p in (0, 1)]
     hook(1)
-    if L.query_schedule(d, 0)[0] == 5:
-        rows["small"] = [time_pass(xs, dzs, g, bt, p) for p in (0, 1)]
+    for r in (4, 8):
+        hook_r(r)
+        if L.query_schedule(d, 0)[0] == 5:
+            rows[f"small_R{r}"] = [time_pass(xs, dzs, g, bt, p) for p in (0, 1)]
+    hook_r(0)
     hook(0)
+    rows["auto"] = [time_pass(xs, dzs, g, bt, p) for p in (0, 1)]
     res[sh] = rows
     print(sh, json.dumps(rows), flush=True)
 print(json.dumps(dict(dtype=args.dtype, N=args.N, **res)))
