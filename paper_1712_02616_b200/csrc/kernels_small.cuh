@@ -66,7 +66,7 @@ __device__ __forceinline__ uint4 ldg_coherent(const void* p) {
 }
 
 template <typename T, int PASS, int R>
-__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? 4 : 3) : (PASS == 0 ? 3 : 2))
+__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2))
     small_kernel(const SmallArgs a) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
