@@ -407,14 +407,20 @@ def preflight_child(args, wl):
     sys.exit(0 if e.item() <= tol else 3)
 
 
+def preflight_env(environ) -> dict:
+    """Environment of a preflight child: a fresh rendezvous on another port; torchrun's
+    agent store (which the parent's process group uses when TORCHELASTIC_USE_AGENT_STORE is
+    set) must not be reused."""
+    env = {k: v for k, v in environ.items() if not k.startswith("TORCHELASTIC")}
+    env["MASTER_PORT"] = str(int(environ.get("MASTER_PORT", "29500")) + 17)
+    return env
+
+
 def preflight_fused(args, pl) -> tuple[bool, str]:
     """Every rank runs preflight_child in a subprocess (its own NCCL group on another
     port); the fused path is used only if every child exits 0."""
     import subprocess
-    # a fresh rendezvous of the children on another port; torchrun's agent store (which the
-    # parent's process group uses when TORCHELASTIC_USE_AGENT_STORE is set) must not be reused
-    env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC")}
-    env["MASTER_PORT"] = str(int(os.environ.get("MASTER_PORT", "29500")) + 17)
+    env = preflight_env(os.environ)
     cmd = [sys.executable, os.path.abspath(__file__), "--preflight-fused", "--config", args.config]
     try:
         r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300)

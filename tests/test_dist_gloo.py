@@ -119,7 +119,28 @@ def _max_timing(rank, world):
     return max_over_ranks([1.0 + rank, 5.0 - rank], "cpu", dist, world)
 
 
+def _dist_plumb(rank, world):
+    """bench.py's N > 1 plumbing (DistPlumb): barrier and element-wise max over ranks."""
+    from bench import DistPlumb
+    pl = DistPlumb(rank, world, "cpu")
+    pl.barrier()
+    m = pl.allmax([float(rank), 10.0 - rank, -1.0 * rank])
+    pl.barrier()
+    return m
+
+
 # ---------------------------------------------------------------- tests
+def test_bench_dist_plumb():
+    out = _run(_dist_plumb)
+    assert out[0] == out[1] == [1.0, 10.0, 0.0]
+
+
+def test_bench_preflight_env():
+    from bench import preflight_env
+    env = preflight_env({"MASTER_PORT": "29500", "RANK": "1", "TORCHELASTIC_USE_AGENT_STORE": "True",
+                         "TORCHELASTIC_RUN_ID": "x", "WORLD_SIZE": "2"})
+    assert env == {"MASTER_PORT": "29517", "RANK": "1", "WORLD_SIZE": "2"}
+
 def test_unique_id_broadcast():
     out = _run(_id_broadcast)
     assert out == {0: True, 1: True}
