@@ -548,9 +548,9 @@ unsigned int* dyn_counters(cudaStream_t st) {
         cudaGetLastError();
         return nullptr;
     }
-    unsigned int* p = nullptr;
-    if (cudaMalloc(&p, 2 * sizeof(unsigned int)) != cudaSuccess ||
-        cudaMemsetAsync(p, 0, 2 * sizeof(unsigned int), st) != cudaSuccess) {
+    unsigned int* p = nullptr;  // [kMaxRanks][2]: one pair per (virtual) rank
+    if (cudaMalloc(&p, 2 * kMaxRanks * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemsetAsync(p, 0, 2 * kMaxRanks * sizeof(unsigned int), st) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
@@ -573,6 +573,19 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         const int dyn = env_int("IABN_FUSED_DYN", 1);
         const size_t slice = (size_t)p.cap * 16u * (pass == 0 ? 1u : 2u);
         if (dyn && p.minb == 2 && (int64_t)p.clusters < a.C && (slice >= 32768 || dyn == 2))
+            a.dyn = dyn_counters(st);
+    } else {
+        // synchronized variant, opt-in (env IABN_SYNC_DYN=1): each rank draws its channels
+        // from its own counter in increasing order, which keeps the cross-rank waits
+        // deadlock-free (the smallest channel not yet finished everywhere has been drawn and
+        // published by every rank).  Measured slower than the static
+        // order at G >= 2 (WideResNet-38 emulated G = 2/4/8: 86.5/86.8/84.3 -> 83.7/80.5/
+        // 75.2 %): with identical static orders the ranks reach a channel at about the same
+        // time; with per-rank dynamic orders a channel's records wait for the slowest rank's
+        // cluster that happens to draw it.
+        const int dyn = env_int("IABN_SYNC_DYN", 0);
+        const size_t slice = (size_t)p.cap * 16u * (pass == 0 ? 1u : 2u);
+        if (dyn && p.minb == 2 && (int64_t)a.qv < a.C && (slice >= 32768 || dyn == 2))
             a.dyn = dyn_counters(st);
     }
     g_last_dyn.store(a.dyn != nullptr ? 1 : 0);

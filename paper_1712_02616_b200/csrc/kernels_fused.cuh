@@ -96,8 +96,9 @@ struct FusedArgs {
                      // into `trace`
     unsigned long long* trace;  // [grid][max_ch][8] %globaltimer ns (debug & 4)
     uint32_t trace_ch;          // channels per CTA recorded
-    // dynamic channel scheduling (one rank): [0] ticket counter, [1] clusters finished;
-    // zero at launch, reset by the last cluster; nullptr = static (cluster q: q, q + Q, ..)
+    // dynamic channel scheduling: per (virtual) rank [2 vr] ticket counter, [2 vr + 1]
+    // clusters finished; zero at launch, reset by the rank's last cluster; nullptr = static
+    // (cluster q: q, q + Q, ..)
     unsigned int* dyn;
 };
 constexpr int kChanRing = 16;  // channel numbers in flight per CTA (dynamic scheduling)
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             auto publish = [&](uint32_t u) {  // CTA 0, lane 0
                 uint32_t c = C;
                 if (!exhausted) {
-                    c = u == 0 ? q : Q + atomicAdd(&a.dyn[0], 1u);
+                    c = u == 0 ? q : Q + atomicAdd(&a.dyn[2 * vr], 1u);
                     if (c >= C) {
                         c = C;
                         exhausted = true;
@@ -664,6 +665,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             };
             auto publish = [&](uint32_t t) {  // channel t's K records (all lanes wait)
                 const uint32_t rs = t % kSlots;
+                const uint32_t ct = chan_of(t);
                 mbar_wait(&gathered[rs], (t / kSlots) & 1u);
                 double v[NR];
                 fold_cluster(rs, v);
@@ -671,15 +673,26 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 if (lane == 0) {
 #pragma unroll
                     for (int k = 0; k < NR; ++k) lrec[rs][k] = v[k];
-                    lterm[rs] = terms(q + t * Q);  // loaded ahead of the fold
+                    lterm[rs] = terms(ct);  // loaded ahead of the fold
                 }
                 if (r == 0 && lane < a.nranks)
-                    st_rec<NR>(a.peer[lane] + half + (size_t)(q + t * Q) * a.nranks + myrank, v,
-                               flag);
+                    st_rec<NR>(a.peer[lane] + half + (size_t)ct * a.nranks + myrank, v, flag);
                 pub = t + 1;
             };
-            for (uint32_t s = 0; s < nT; ++s) {
-                const int64_t cp = q + s * Q;
+            // slot t's channel without blocking (dynamic order: CTA 0's producer may not have
+            // drawn it yet -- waiting here could hold up the buffer it needs), C = none
+            auto chan_peek = [&](uint32_t t, bool* known) -> uint32_t {
+                if (!dynamic) {
+                    *known = true;
+                    return t < nT ? q + t * Q : C;
+                }
+                *known = mbar_test(&chanbar[t % kChanRing], (t / kChanRing) & 1u);
+                return *known ? *(volatile uint32_t*)&chan_ring[t % kChanRing] : C;
+            };
+            for (uint32_t s = 0;; ++s) {
+                const uint32_t cs_ = chan_of(s);
+                if (cs_ >= C) break;
+                const int64_t cp = cs_;
                 if (s >= 2) mbar_wait(&freed[s & 1u], (s / 2 - 1) & 1u);
                 while (pub <= s) {
                     if (armed <= pub) arm(pub);
@@ -694,7 +707,9 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     bool ok = true;
                     if (lane < a.nranks) ok = ld_rec<NR>(src, flag, v);
                     if (__all_sync(0xffffffffu, ok)) break;
-                    if (pub < nT && pub < s + kSlots) {
+                    bool known = false;
+                    const uint32_t cpub = pub < s + kSlots ? chan_peek(pub, &known) : C;
+                    if (known && cpub < C) {
                         if (armed <= pub) arm(pub);
                         const bool in = __shfl_sync(
                             0xffffffffu,
@@ -1225,9 +1240,9 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
     if (dynamic && r == 0 && threadIdx.x == 0) {
         // the last cluster (every ticket is drawn by then) re-arms the counters
         __threadfence();
-        if (atomicAdd(&a.dyn[1], 1u) == gridDim.x / K - 1) {
-            atomicExch(&a.dyn[0], 0u);
-            atomicExch(&a.dyn[1], 0u);
+        if (atomicAdd(&a.dyn[2 * vr + 1], 1u) == Q - 1) {  // this rank's clusters
+            atomicExch(&a.dyn[2 * vr], 0u);
+            atomicExch(&a.dyn[2 * vr + 1], 0u);
         }
     }
     if (a.nranks > 1 && threadIdx.x == 0) {

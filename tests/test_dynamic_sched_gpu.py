@@ -100,3 +100,21 @@ def test_dynamic_graph_replay_and_two_streams():
     torch.cuda.synchronize()
     for k in ref:
         assert torch.equal(o1[k], ref[k]) and torch.equal(o2[k], ref[k]), k
+
+
+@pytest.mark.slow
+def test_dynamic_order_forced_on_small_slices_and_sync_emulation():
+    """The dynamic order on every channel-resident launch (IABN_FUSED_DYN=2, IABN_SYNC_DYN=2:
+    also small slices and the fused-collective sync over virtual ranks -- opt-in there --
+    where each rank draws its own increasing channel sequence): the sync-emulation and plain
+    parity suites rerun in a subprocess (the variables are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IABN_FUSED_DYN="2", IABN_SYNC_DYN="2")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        "tests/test_sync_fused_gpu.py", "tests/test_parity_gpu.py",
+                        "-k", "not full_size"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
