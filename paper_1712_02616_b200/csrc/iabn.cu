@@ -583,7 +583,8 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
         // 75.2 %): with identical static orders the ranks reach a channel at about the same
         // time; with per-rank dynamic orders a channel's records wait for the slowest rank's
         // cluster that happens to draw it.
-        const int dyn = env_int("IABN_SYNC_DYN", 0);
+        // (one rank -- the G = 1 emulation -- has no cross-rank waits: dynamic as above)
+        const int dyn = a.nranks <= 1 ? env_int("IABN_FUSED_DYN", 1) : env_int("IABN_SYNC_DYN", 0);
         const size_t slice = (size_t)p.cap * 16u * (pass == 0 ? 1u : 2u);
         if (dyn && p.minb == 2 && (int64_t)a.qv < a.C && (slice >= 32768 || dyn == 2))
             a.dyn = dyn_counters(st);
