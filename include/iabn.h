@@ -99,8 +99,9 @@ enum {
     IABN_EVAL = 1u << 4,
     /* schedule overrides (testing / benchmarking); default = automatic */
     IABN_FORCE_STREAMING = 1u << 8, /* multi-kernel streaming schedule */
-    IABN_FORCE_FUSED = 1u << 9,     /* channel-resident cluster schedule; IABN_ERR_UNSUPPORTED
-                                       when the shape does not fit on chip */
+    IABN_FORCE_FUSED = 1u << 9,     /* channel-resident cluster schedule (NCHW; for NHWC the
+                                       channel-group schedule); IABN_ERR_UNSUPPORTED when the
+                                       shape does not fit on chip */
     /* 1u << 10: reserved (was a one-launch cooperative variant of the streaming schedule,
        measured slower than three launches on every shape and removed) */
     IABN_FORCE_RESIDENT = 1u << 11,   /* NHWC: the whole tensor resident in the grid's shared
@@ -133,8 +134,10 @@ IABN_API uint64_t iabn_launch_count(void);
 /* Workspace bytes needed by every call on `desc` (0 if desc is invalid). */
 IABN_API size_t iabn_workspace_bytes(const iabn_desc *desc);
 /* Schedule the library would use: pass 0 = forward, 1 = backward.  On return
-   *schedule is 0 (streaming), 1 (channel-resident fused) or 3 (grid-resident NHWC:
-   the whole tensor in the grid's shared memory; 2 is no longer returned),
+   *schedule is 0 (streaming), 1 (channel-resident fused), 3 (grid-resident NHWC:
+   the whole tensor in the grid's shared memory), 4 (NHWC channel groups: a cluster holds
+   a column group of all rows, 2-D TMA) or 5 (small NCHW layers held in registers); 2 is
+   no longer returned,
    *cluster the CTAs per channel of the fused schedule (0 otherwise). */
 IABN_API iabn_status iabn_query_schedule(const iabn_desc *desc, int pass, uint32_t flags, int *schedule,
                                 int *cluster);
