@@ -527,6 +527,23 @@ def run_rank(args, wl, pl, make_comm, emulated: bool):
         out["allreduce_ms_per_step"] = round(ar_ms, 4)
         out["allreduce_pct_of_step"] = round(100 * ar_ms / max(sum(med), 1e-9), 2)
         out["messages_bytes"] = {"forward_stats_fp64": 24 * C, "backward_sums_fp64": 8 * (2 * C + 1)}
+        if not emulated:
+            # context: a standalone NCCL all-reduce of the same messages (torch.distributed,
+            # same process group, device-timed, max over ranks)
+            import torch.distributed as dist
+            sa = {}
+            for name, n in (("forward_stats_fp64", 3 * C), ("backward_sums_fp64", 2 * C + 1)):
+                buf = torch.zeros(n, dtype=torch.float64, device=dev)
+                for _ in range(5):
+                    dist.all_reduce(buf)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                for _ in range(50):
+                    dist.all_reduce(buf)
+                e1.record(st)
+                torch.cuda.synchronize()
+                sa[name] = round(pl.allmax([e0.elapsed_time(e1) / 50 * 1e3])[0], 2)
+            out["nccl_standalone_us"] = sa
         return out
 
     def result(m):
