@@ -23,6 +23,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 GAMMA_MODES = {"abs_eps": 0, "plain": 1, "fixed_one": 2}
+ACTS = {"leaky": 0, "sigmoid": 1, "tanh": 2}
 LAYOUTS = {"NCHW": 0, "NHWC": 1}
 
 _D = ctypes.POINTER(ctypes.c_double)
@@ -65,6 +66,14 @@ def _bind(lib: ctypes.CDLL) -> ctypes.CDLL:
     lib.oracle_param_grads_sharded.argtypes = [_I64, _I64, _I64, i, _D, _D, _D, _D, i, d, d, _I64,
                                                ctypes.POINTER(_I64), _D, _D]
     lib.oracle_param_grads_sharded.restype = None
+    lib.oracle_forward_act.argtypes = [_I64, _I64, _I64, i, _D, _D, _D, i, d, i, d, _D, _D, _D]
+    lib.oracle_backward_standard_act.argtypes = [_I64, _I64, _I64, i, _D, _D, _D, _D, i, d, i,
+                                                 d, _D, _D, _D]
+    lib.oracle_backward_inplace_act.argtypes = [_I64, _I64, _I64, i, _D, _D, _D, _D, _D, i, d, i,
+                                                d, _D, _D, _D]
+    for f in (lib.oracle_forward_act, lib.oracle_backward_standard_act,
+              lib.oracle_backward_inplace_act):
+        f.restype = None
     lib.oracle_mutant_id.restype = ctypes.c_int
     return lib
 
@@ -201,6 +210,40 @@ class Oracle:
                                             GAMMA_MODES[gamma_mode], eps, slope, K, sn, _p(dg),
                                             _p(db))
         return dg, db
+
+    # ------------------------------------------- other invertible activations
+    def forward_act(self, x, gamma, beta, *, act="sigmoid", eps=1e-5, slope=0.01,
+                    gamma_mode="abs_eps", layout="NCHW"):
+        """(z, mean, biased var) of BN followed by `act` (leaky / sigmoid / tanh)."""
+        x = _f64(x)
+        N, C, HW = _shape(x, layout)
+        z, mean, var = np.empty_like(x), np.empty(C), np.empty(C)
+        self.lib.oracle_forward_act(N, C, HW, LAYOUTS[layout], _p(x), _p(_f64(gamma)),
+                                    _p(_f64(beta)), GAMMA_MODES[gamma_mode], eps, ACTS[act],
+                                    slope, _p(z), _p(mean), _p(var))
+        return z, mean, var
+
+    def backward_standard_act(self, x, dz, gamma, beta, *, act="sigmoid", eps=1e-5, slope=0.01,
+                              gamma_mode="abs_eps", layout="NCHW"):
+        x, dz = _f64(x), _f64(dz)
+        N, C, HW = _shape(x, layout)
+        dx, dg, db = np.empty_like(x), np.empty(C), np.empty(C)
+        self.lib.oracle_backward_standard_act(N, C, HW, LAYOUTS[layout], _p(x), _p(dz),
+                                              _p(_f64(gamma)), _p(_f64(beta)),
+                                              GAMMA_MODES[gamma_mode], eps, ACTS[act], slope,
+                                              _p(dx), _p(dg), _p(db))
+        return dx, dg, db
+
+    def backward_inplace_act(self, z, dz, var, gamma, beta, *, act="sigmoid", eps=1e-5,
+                             slope=0.01, gamma_mode="abs_eps", layout="NCHW"):
+        z, dz = _f64(z), _f64(dz)
+        N, C, HW = _shape(z, layout)
+        dx, dg, db = np.empty_like(z), np.empty(C), np.empty(C)
+        self.lib.oracle_backward_inplace_act(N, C, HW, LAYOUTS[layout], _p(z), _p(dz),
+                                             _p(_f64(var)), _p(_f64(gamma)), _p(_f64(beta)),
+                                             GAMMA_MODES[gamma_mode], eps, ACTS[act], slope,
+                                             _p(dx), _p(dg), _p(db))
+        return dx, dg, db
 
     def merge_stats(self, counts, means, vars_):
         counts, means, vars_ = _f64(counts), _f64(means), _f64(vars_)

@@ -462,4 +462,148 @@ void oracle_param_grads_sharded(int64_t N, int64_t C, int64_t HW, int layout, co
     }
 }
 
+/*
+ * Other invertible activations ("Many activation functions are actually
+ * invertible and can be computed in-place (e.g. sigmoid, hyperbolic tangent, Leaky ReLU,
+ * and others)").  act: ORACLE_ACT_LEAKY (slope a), ORACLE_ACT_SIGMOID, ORACLE_ACT_TANH.
+ *   sigmoid: f(y) = 1/(1 + e^-y), f'(y) = f(y)(1 - f(y)), f^-1(z) = log(z/(1 - z))
+ *   tanh:    f(y) = tanh(y),      f'(y) = 1 - f(y)^2,    f^-1(z) = atanh(z)
+ */
+static double act_f(int act, double y, double a)
+{
+    if (act == ORACLE_ACT_SIGMOID)
+        return 1.0 / (1.0 + exp(-y));
+    if (act == ORACLE_ACT_TANH)
+        return tanh(y);
+    return leaky(y, a);
+}
+/* f'(y) computed from z = f(y) (Alg. 2 l.2: the backward sees only z) */
+static double act_deriv_z(int act, double z, double a)
+{
+#if ORACLE_MUTANT == 14
+    if (act == ORACLE_ACT_SIGMOID)
+        return z * (1.0 + z); /* mutant: sign slip in the sigmoid derivative */
+#else
+    if (act == ORACLE_ACT_SIGMOID)
+        return z * (1.0 - z);
+#endif
+    if (act == ORACLE_ACT_TANH)
+        return 1.0 - z * z;
+    return leaky_deriv(z, a);
+}
+static double act_inv(int act, double z, double a)
+{
+    if (act == ORACLE_ACT_SIGMOID)
+        return log(z / (1.0 - z));
+    if (act == ORACLE_ACT_TANH)
+        return atanh(z);
+    return leaky_inv(z, a);
+}
+
+/* Forward of BN followed by activation `act` from stored x (as oracle_forward, without
+ * running statistics): z = act(gamma~ (x - mu) rstd + beta). */
+void oracle_forward_act(int64_t N, int64_t C, int64_t HW, int layout, const double *x,
+                        const double *gamma, const double *beta, int gamma_mode, double eps,
+                        int act, double slope, double *z, double *mean_out, double *var_out)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < C; ++c) {
+        double mu, var;
+        channel_stats(N, C, HW, layout, x, c, &mu, &var);
+        const double rstd = 1.0 / sqrt(var + eps);
+        const double g = gamma_eff(gamma_mode, gamma[c], eps);
+        for (int64_t n = 0; n < N; ++n)
+            for (int64_t s = 0; s < HW; ++s) {
+                const size_t i = at(layout, C, HW, n, c, s);
+                z[i] = act_f(act, g * (x[i] - mu) * rstd + beta[c], slope);
+            }
+        if (mean_out)
+            mean_out[c] = mu;
+        if (var_out)
+            var_out[c] = var;
+    }
+}
+
+/* Backward from STORED x for activation `act` (the chain rule of oracle_backward_standard,
+ * PAPER.md:428-449, with dy = f'(y) dz, f'(y) from f(y) as written above). */
+void oracle_backward_standard_act(int64_t N, int64_t C, int64_t HW, int layout,
+                                  const double *x, const double *dz, const double *gamma,
+                                  const double *beta, int gamma_mode, double eps, int act,
+                                  double slope, double *dx, double *dgamma, double *dbeta)
+{
+    const double m = (double)(N * HW);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < C; ++c) {
+        double mu, var;
+        channel_stats(N, C, HW, layout, x, c, &mu, &var);
+        const double rstd = 1.0 / sqrt(var + eps);
+        const double g = gamma_eff(gamma_mode, gamma[c], eps);
+        double sdy = 0.0, sdyxh = 0.0, sdvar = 0.0, sdxh = 0.0, sxm = 0.0;
+        for (int64_t n = 0; n < N; ++n)
+            for (int64_t s = 0; s < HW; ++s) {
+                const size_t i = at(layout, C, HW, n, c, s);
+                const double xm = x[i] - mu;
+                const double xhat = xm * rstd;
+                const double fy = act_f(act, g * xhat + beta[c], slope);
+                const double dy = (act == ORACLE_ACT_SIGMOID ? fy * (1.0 - fy)
+                                   : act == ORACLE_ACT_TANH ? 1.0 - fy * fy
+                                   : leaky_deriv(g * xhat + beta[c], slope)) * dz[i];
+                const double dxhat = dy * g;
+                sdy += dy;
+                sdyxh += dy * xhat;
+                sdvar += dxhat * xm;
+                sdxh += dxhat;
+                sxm += xm;
+            }
+        const double dvar = sdvar * (-0.5) * pow(var + eps, -1.5);
+        const double dmu = sdxh * (-rstd) + dvar * (-2.0 / m) * sxm;
+        for (int64_t n = 0; n < N; ++n)
+            for (int64_t s = 0; s < HW; ++s) {
+                const size_t i = at(layout, C, HW, n, c, s);
+                const double xm = x[i] - mu;
+                const double y = g * xm * rstd + beta[c];
+                const double fy = act_f(act, y, slope);
+                const double dy = (act == ORACLE_ACT_SIGMOID ? fy * (1.0 - fy)
+                                   : act == ORACLE_ACT_TANH ? 1.0 - fy * fy
+                                   : leaky_deriv(y, slope)) * dz[i];
+                dx[i] = dy * g * rstd + dvar * 2.0 * xm / m + dmu / m;
+            }
+        dbeta[c] = sdy;
+        dgamma[c] = sdyxh * gamma_eff_deriv(gamma_mode, gamma[c]);
+    }
+}
+
+/* InPlace-ABN I backward from the stored z for activation `act` (Alg. 2 l.2-6,
+ * PAPER.md:215-223): dy = f'(z) dz, x^ = (f^-1(z) - beta)/gamma~, BN* (PAPER.md:168). */
+void oracle_backward_inplace_act(int64_t N, int64_t C, int64_t HW, int layout, const double *z,
+                                 const double *dz, const double *var, const double *gamma,
+                                 const double *beta, int gamma_mode, double eps, int act,
+                                 double slope, double *dx, double *dgamma, double *dbeta)
+{
+    const double m = (double)(N * HW);
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < C; ++c) {
+        const double rstd = 1.0 / sqrt(var[c] + eps);
+        const double g = gamma_eff(gamma_mode, gamma[c], eps);
+        double sdy = 0.0, sdyxh = 0.0;
+        for (int64_t n = 0; n < N; ++n)
+            for (int64_t s = 0; s < HW; ++s) {
+                const size_t i = at(layout, C, HW, n, c, s);
+                const double dy = act_deriv_z(act, z[i], slope) * dz[i];
+                const double xhat = (act_inv(act, z[i], slope) - beta[c]) / g;
+                sdy += dy;
+                sdyxh += dy * xhat;
+            }
+        for (int64_t n = 0; n < N; ++n)
+            for (int64_t s = 0; s < HW; ++s) {
+                const size_t i = at(layout, C, HW, n, c, s);
+                const double dy = act_deriv_z(act, z[i], slope) * dz[i];
+                const double xhat = (act_inv(act, z[i], slope) - beta[c]) / g;
+                dx[i] = (dy - sdyxh * xhat / m - sdy / m) * g * rstd;
+            }
+        dbeta[c] = sdy;
+        dgamma[c] = sdyxh * gamma_eff_deriv(gamma_mode, gamma[c]);
+    }
+}
+
 int oracle_mutant_id(void) { return ORACLE_MUTANT; }

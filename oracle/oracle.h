@@ -13,6 +13,10 @@
 #define ORACLE_GAMMA_PLAIN 1     /* gamma~ = gamma */
 #define ORACLE_GAMMA_FIXED_ONE 2 /* gamma~ = 1 */
 
+#define ORACLE_ACT_LEAKY 0   /* leaky ReLU with slope a (the paper's choice) */
+#define ORACLE_ACT_SIGMOID 1
+#define ORACLE_ACT_TANH 2
+
 void oracle_channel_stats(int64_t N, int64_t C, int64_t HW, int layout, const double *x,
                           double *mean, double *var);
 void oracle_forward(int64_t N, int64_t C, int64_t HW, int layout, const double *x,
@@ -47,5 +51,16 @@ void oracle_param_grads_sharded(int64_t N, int64_t C, int64_t HW, int layout, co
                                 const double *dz, const double *gamma, const double *beta,
                                 int gamma_mode, double eps, double slope, int64_t nshards,
                                 const int64_t *shard_n, double *dgamma, double *dbeta);
+void oracle_forward_act(int64_t N, int64_t C, int64_t HW, int layout, const double *x,
+                        const double *gamma, const double *beta, int gamma_mode, double eps,
+                        int act, double slope, double *z, double *mean_out, double *var_out);
+void oracle_backward_standard_act(int64_t N, int64_t C, int64_t HW, int layout,
+                                  const double *x, const double *dz, const double *gamma,
+                                  const double *beta, int gamma_mode, double eps, int act,
+                                  double slope, double *dx, double *dgamma, double *dbeta);
+void oracle_backward_inplace_act(int64_t N, int64_t C, int64_t HW, int layout, const double *z,
+                                 const double *dz, const double *var, const double *gamma,
+                                 const double *beta, int gamma_mode, double eps, int act,
+                                 double slope, double *dx, double *dgamma, double *dbeta);
 int oracle_mutant_id(void);
 #endif

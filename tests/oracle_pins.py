@@ -335,6 +335,47 @@ def pin_sharded_param_grads(o):
                 assert vec_err(hg[k], dg) < 1e-12 and vec_err(hb[k], db) < 1e-12
 
 
+def pin_act_torch_f64(o):
+    """Other invertible activations: BN + sigmoid / tanh from stored x against
+    PyTorch float64 (F.batch_norm, torch.sigmoid / torch.tanh, autograd), both layouts."""
+    for act, fn in (("sigmoid", torch.sigmoid), ("tanh", torch.tanh)):
+        for layout in ("NCHW", "NHWC"):
+            x, dz, gamma, beta = _rand_problem(4, 5, 9, seed=31, layout=layout)
+            z, mean, var = o.forward_act(x, gamma, beta, act=act, layout=layout)
+            dx, dg, db = o.backward_standard_act(x, dz, gamma, beta, act=act, layout=layout)
+            xt = torch.tensor(x if layout == "NCHW" else np.transpose(x, (0, 2, 1)),
+                              requires_grad=True)
+            gt = torch.tensor(gamma, requires_grad=True)
+            bt = torch.tensor(beta, requires_grad=True)
+            geff = gt.abs() + 1e-5
+            zt = fn(F.batch_norm(xt, None, None, weight=geff, bias=bt, training=True, eps=1e-5))
+            dzt = torch.tensor(dz if layout == "NCHW" else np.transpose(dz, (0, 2, 1)))
+            zt.backward(dzt)
+            tr = (lambda a: a) if layout == "NCHW" else (lambda a: np.transpose(a, (0, 2, 1)))
+            assert chan_err(z, tr(zt.detach().numpy()), 1 if layout == "NCHW" else 2) < 1e-12
+            assert chan_err(dx, tr(xt.grad.numpy()), 1 if layout == "NCHW" else 2) < 1e-10
+            assert vec_err(dg, gt.grad.numpy()) < 1e-10 and vec_err(db, bt.grad.numpy()) < 1e-10
+
+
+def pin_act_inplace_equals_stored_x(o):
+    """Alg. 2 from z (f^-1, f' from z) equals the stored-x chain rule for sigmoid / tanh
+    (the invariant of BASELINE.json: 'gradient via inversion of z equals gradient via
+    stored x'); with act = leaky it reduces to oracle_backward_inplace_I."""
+    for act in ("sigmoid", "tanh", "leaky"):
+        x, dz, gamma, beta = _rand_problem(5, 4, 8, seed=32)
+        z, mean, var = o.forward_act(x, gamma, beta, act=act)
+        a = o.backward_standard_act(x, dz, gamma, beta, act=act)
+        b = o.backward_inplace_act(z, dz, var, gamma, beta, act=act)
+        for u, v in zip(a, b):
+            assert rel_err(v, u) < 1e-9, act
+    x, dz, gamma, beta = _rand_problem(5, 4, 8, seed=33)
+    f = o.forward(x, gamma, beta)
+    ref = o.backward_inplace_I(f.z, dz, f.var, gamma, beta)
+    got = o.backward_inplace_act(f.z, dz, f.var, gamma, beta, act="leaky")
+    for u, v in zip(ref, got):
+        assert rel_err(v, u) < 1e-14
+
+
 def pin_permute_batch(o):
     x, dz, gamma, beta = _rand_problem(5, 4, 6, seed=12)
     perm = np.array([3, 0, 4, 1, 2])
@@ -384,4 +425,4 @@ PINS = [pin_golden_bn, pin_golden_leaky, pin_golden_running, pin_golden_running_
         pin_golden_sync, pin_sharded_param_grads, pin_whitening,
         pin_const_dz, pin_dx_moments, pin_torch_f64, pin_torch_eval, pin_finite_diff,
         pin_three_way, pin_fixed_one, pin_scaling, pin_sync_concat, pin_permute_batch,
-        pin_golden_fold, pin_fold_conv]
+        pin_golden_fold, pin_fold_conv, pin_act_torch_f64, pin_act_inplace_equals_stored_x]

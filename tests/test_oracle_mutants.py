@@ -6,7 +6,7 @@ import pytest
 import oracle
 from tests.oracle_pins import PINS
 
-MUTANTS = list(range(1, 14))
+MUTANTS = list(range(1, 15))
 
 
 @pytest.mark.parametrize("mutant", MUTANTS)
