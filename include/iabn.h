@@ -110,7 +110,18 @@ enum {
     /* iabn_{forward,backward}_sync: the channel-resident kernels with the cross-rank
        exchange inside the kernel (see "fused-collective sync" below) instead of reduce
        kernels + ncclAllReduce + apply kernels.  Also enabled by env IABN_SYNC_FUSED=1. */
-    IABN_SYNC_FUSED = 1u << 12
+    IABN_SYNC_FUSED = 1u << 12,
+    /* Activation f after BN ("sigmoid, hyperbolic tangent, Leaky ReLU, and
+       others" are invertible): default leaky ReLU with `slope`; these two select
+       f = sigmoid or f = tanh (slope ignored), exclusive.  iabn_forward / iabn_backward
+       only (the split-phase and synchronized entries return IABN_ERR_UNSUPPORTED), fp32
+       storage only (IABN_ERR_UNSUPPORTED for bf16: the inverse of an 8-bit-mantissa
+       sigmoid / tanh output is ill-conditioned), streaming schedule (the FORCE flags are
+       ignored).  The backward inverts z: x^ = (f^-1(z) - beta)/g, dy = f'(z) dz (Alg. 2),
+       with z clamped into the open range of f first (saturated outputs, R17);
+       IABN_VARIANT_I makes no difference here. */
+    IABN_ACT_SIGMOID = 1u << 13,
+    IABN_ACT_TANH = 1u << 14
 };
 
 typedef struct iabn_desc {

@@ -29,6 +29,8 @@ FORCE_STREAMING = 1 << 8
 FORCE_FUSED = 1 << 9
 FORCE_RESIDENT = 1 << 11
 SYNC_FUSED = 1 << 12
+ACT_SIGMOID = 1 << 13
+ACT_TANH = 1 << 14
 
 EXPORTS = ["iabn_version", "iabn_status_string", "iabn_last_error", "iabn_launch_count",
            "iabn_workspace_bytes", "iabn_query_schedule", "iabn_forward", "iabn_backward",

@@ -23,6 +23,7 @@
 #include <string>
 
 #include "iabn.h"
+#include "kernels_act.cuh"
 #include "kernels_gres.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_nhwc.cuh"
@@ -1660,10 +1661,115 @@ iabn_status emu_sync_buf(cudaStream_t st, int G, int64_t C, SyncBuf* out) {
     return IABN_OK;
 }
 
+// ====================================================================== other activations
+// BN + sigmoid / tanh (kernels_act.cuh): the streaming schedule only.
+uint32_t act_of(uint32_t flags) { return flags & (IABN_ACT_SIGMOID | IABN_ACT_TANH); }
+
+iabn_status check_act_flags(const Geom& g, uint32_t flags) {
+    const uint32_t a = act_of(flags);
+    if (!a) return IABN_OK;
+    if (a == (IABN_ACT_SIGMOID | IABN_ACT_TANH))
+        return fail(IABN_ERR_INVALID_ARG, "IABN_ACT_SIGMOID and IABN_ACT_TANH are exclusive");
+    if (g.dtype != IABN_F32)
+        return fail(IABN_ERR_UNSUPPORTED,
+                    "sigmoid / tanh need fp32 storage (their inverse is ill-conditioned on an "
+                    "8-bit mantissa)");
+    return IABN_OK;
+}
+
+template <int ACT>
+iabn_status act_elementwise(const Geom& g, int pass, const float* in0, const float* in1,
+                            float* out, const float4* coef, int sms, cudaStream_t st) {
+    const int64_t spc = samples_per_chunk(g);
+    if (spc <= 0) return fail(IABN_ERR_UNSUPPORTED, "sample too large for the streaming apply");
+    const FastDiv fh = fd32(g.HW), fc = fd32(g.C);
+    for (int64_t n0 = 0; n0 < g.N; n0 += spc) {
+        const int64_t nn = std::min(spc, g.N - n0);
+        const int64_t off = n0 * g.C * g.HW;
+        const uint32_t E = (uint32_t)(nn * g.C * g.HW);
+        const int grid = apply_grid(E, 4, sms);
+        const bool al = g.layout == IABN_NCHW ? g.HW % 4 == 0 : g.C % 4 == 0;
+        const int fixed = g.layout == IABN_NHWC && al ? nhwc_grid(g, E / 4, sms) : 0;
+        const float *a = in0 + off, *b = in1 ? in1 + off : nullptr;
+        float* o = out + off;
+#define IABN_ACT_LAUNCH(P, LY, AL) \
+    launch_pdl(act_apply_kernel<ACT, P, LY, AL>, grid, kThreads, 0, st, a, b, o, coef, E, fh, fc)
+        if (pass == 0) {
+            if (g.layout == IABN_NCHW) { if (al) IABN_ACT_LAUNCH(0, 0, true); else IABN_ACT_LAUNCH(0, 0, false); }
+            else if (fixed) launch_pdl(act_apply_fixed_kernel<ACT, 0>, fixed, kThreads, 0, st, a, b, o, coef, E, fh, fc);
+            else { if (al) IABN_ACT_LAUNCH(0, 1, true); else IABN_ACT_LAUNCH(0, 1, false); }
+        } else {
+            if (g.layout == IABN_NCHW) { if (al) IABN_ACT_LAUNCH(1, 0, true); else IABN_ACT_LAUNCH(1, 0, false); }
+            else if (fixed) launch_pdl(act_apply_fixed_kernel<ACT, 1>, fixed, kThreads, 0, st, a, b, o, coef, E, fh, fc);
+            else { if (al) IABN_ACT_LAUNCH(1, 1, true); else IABN_ACT_LAUNCH(1, 1, false); }
+        }
+#undef IABN_ACT_LAUNCH
+        IABN_TRY(check_launch(pass == 0 ? "act_fwd_apply kernel" : "act_bwd_apply kernel"));
+    }
+    return IABN_OK;
+}
+
+template <int ACT>
+iabn_status act_reduce(const Geom& g, int S, const float* z, const float* dz, const float* gamma,
+                       const float* beta, float eps, uint32_t flags, double* part, cudaStream_t st) {
+    if (g.layout == IABN_NCHW && g.HW % 4 == 0)
+        launch_pdl(act_bwd_reduce_nchw_kernel<ACT, true>, dim3((unsigned)g.C, (unsigned)S), kThreads, 0, st,
+            z, dz, gamma, beta, g.C, (uint32_t)g.HW, (uint32_t)g.m, fd32(g.HW / 4), eps, flags, part);
+    else if (g.layout == IABN_NCHW)
+        launch_pdl(act_bwd_reduce_nchw_kernel<ACT, false>, dim3((unsigned)g.C, (unsigned)S), kThreads, 0, st,
+            z, dz, gamma, beta, g.C, (uint32_t)g.HW, (uint32_t)g.m, fd32(g.HW), eps, flags, part);
+    else if (g.C % 4 == 0)
+        launch_pdl(act_bwd_reduce_nhwc_kernel<ACT>, dim3((unsigned)((g.C + 63) / 64), (unsigned)S), kThreads, 0, st,
+            z, dz, gamma, beta, g.C, g.m, eps, flags, part);
+    else
+        launch_pdl(act_bwd_reduce_nhwc_scalar_kernel<ACT>, dim3((unsigned)((g.C + 31) / 32), (unsigned)S), kThreads, 0, st,
+            z, dz, gamma, beta, g.C, g.m, eps, flags, part);
+    return check_launch("act_bwd_reduce kernel");
+}
+
+iabn_status act_forward(const Ctx& c, const float* x, float* z, const float* gamma,
+                        const float* beta, float* rm, float* rv, float* sm, float* sv,
+                        float momentum, float eps, uint32_t flags) {
+    float4* coef = wsp<float4>(c, c.w.coef);
+    if (flags & IABN_EVAL) {
+        launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv, eps, flags, coef);
+        IABN_TRY(check_launch("eval_coef kernel"));
+    } else {
+        IABN_TRY(launch_stats<float>(c.g, c.S, x, wsp<double>(c, c.w.part), c.st));
+        FwdCoefArgs a{wsp<double>(c, c.w.part), c.S, c.g.C, gamma, beta, rm, rv, sm, sv, coef,
+                      momentum, eps, flags};
+        launch_pdl(fwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
+        IABN_TRY(check_launch("fwd_coef kernel"));
+    }
+    return (flags & IABN_ACT_SIGMOID)
+               ? act_elementwise<1>(c.g, 0, x, nullptr, z, coef, c.dev->sms, c.st)
+               : act_elementwise<2>(c.g, 0, x, nullptr, z, coef, c.dev->sms, c.st);
+}
+
+iabn_status act_backward(const Ctx& c, const float* z, const float* dz, float* dx,
+                         const float* gamma, const float* beta, const float* sv, float* dg,
+                         float* db, float eps, uint32_t flags) {
+    double* part = wsp<double>(c, c.w.part);
+    float4* coef = wsp<float4>(c, c.w.coef);
+    const bool sig = flags & IABN_ACT_SIGMOID;
+    IABN_TRY(sig ? act_reduce<1>(c.g, c.S, z, dz, gamma, beta, eps, flags, part, c.st)
+                 : act_reduce<2>(c.g, c.S, z, dz, gamma, beta, eps, flags, part, c.st));
+    BwdCoefArgs a{part, c.S, part, c.S, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg, db,
+                  coef, eps, flags};
+    launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
+    IABN_TRY(check_launch("bwd_coef kernel"));
+    return sig ? act_elementwise<1>(c.g, 1, z, dz, dx, coef, c.dev->sms, c.st)
+               : act_elementwise<2>(c.g, 1, z, dz, dx, coef, c.dev->sms, c.st);
+}
+
 template <typename T>
 iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamma,
                          const float* beta, float* rm, float* rv, float* sm, float* sv,
                          float momentum, float eps, float slope, uint32_t flags) {
+    if constexpr (std::is_same<T, float>::value)
+        if (act_of(flags))
+            return act_forward(c, (const float*)x, (float*)z, gamma, beta, rm, rv, sm, sv,
+                               momentum, eps, flags);
     if (flags & IABN_EVAL) {
         launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv, eps, flags,
                                                          wsp<float4>(c, c.w.coef));
@@ -1757,6 +1863,10 @@ template <typename T>
 iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
                           const float* gamma, const float* beta, const float* sv, float* dg,
                           float* db, float eps, float slope, uint32_t flags) {
+    if constexpr (std::is_same<T, float>::value)
+        if (act_of(flags))
+            return act_backward(c, (const float*)z, (const float*)dz, (float*)dx, gamma, beta, sv,
+                                dg, db, eps, flags);
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
         const SmallPlan sp = small_plan(c.g, flags);
         if (sp.ok) {
@@ -1935,6 +2045,12 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     if (pass != 0 && pass != 1) return fail(IABN_ERR_INVALID_ARG, "pass must be 0 or 1");
     DevFacts* dev;
     IABN_TRY(device_facts(&dev));
+    if (act_of(flags)) {  // sigmoid / tanh: streaming only
+        IABN_TRY(check_act_flags(g, flags));
+        *schedule = 0;
+        *cluster = 0;
+        return IABN_OK;
+    }
     if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
         const SmallPlan sp = small_plan(g, flags);
         if (sp.ok) {
@@ -1967,6 +2083,7 @@ iabn_status iabn_forward(const iabn_desc* desc, const void* x, void* z, const fl
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     IABN_TRY(validate_fwd(c, x, z, gamma, beta, running_mean, running_var, save_mean, save_var,
                           momentum, eps, slope, flags, c.g.m));
+    IABN_TRY(check_act_flags(c.g, flags));
     IABN_TRY(attach_device(c));
     return fault_after(DISPATCH(c.g.dtype, forward_impl, c, x, z, gamma, beta, running_mean,
                                 running_var, save_mean, save_var, momentum, eps, slope, flags),
@@ -1981,6 +2098,7 @@ iabn_status iabn_backward(const iabn_desc* desc, const void* z, const void* dz, 
     Ctx c;
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
+    IABN_TRY(check_act_flags(c.g, flags));
     IABN_TRY(attach_device(c));
     return fault_after(DISPATCH(c.g.dtype, backward_impl, c, z, dz, dx, gamma, beta, save_var,
                                 dgamma, dbeta, eps, slope, flags),
@@ -2034,6 +2152,7 @@ iabn_status iabn_forward_apply(const iabn_desc* desc, const void* x, void* z,
                                float* running_mean, float* running_var, float* save_mean,
                                float* save_var, float momentum, float eps, float slope,
                                uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     Ctx c;
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     if (!stats_global) return fail(IABN_ERR_INVALID_ARG, "stats_global is NULL");
@@ -2049,6 +2168,7 @@ iabn_status iabn_backward_reduce(const iabn_desc* desc, const void* z, const voi
                                  const float* gamma, const float* beta, double* sums, float eps,
                                  float slope, uint32_t flags, void* ws, size_t ws_bytes,
                                  void* stream) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     Ctx c;
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     IABN_TRY(check_act("z", z));
@@ -2068,6 +2188,7 @@ iabn_status iabn_backward_apply(const iabn_desc* desc, const void* z, const void
                                 const float* gamma, const float* beta, const float* save_var,
                                 float* dgamma, float* dbeta, float eps, float slope,
                                 uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     Ctx c;
     IABN_TRY(make_ctx(desc, ws, ws_bytes, stream, &c));
     IABN_TRY(validate_bwd(c, z, dz, dx, gamma, beta, save_var, dgamma, dbeta, eps, slope));
@@ -2158,6 +2279,7 @@ iabn_status iabn_forward_sync(const iabn_desc* desc, const void* x, void* z, con
                               float* save_mean, float* save_var, float momentum, float eps,
                               float slope, uint32_t flags, void* ws, size_t ws_bytes,
                               void* stream, iabn_comm comm) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     if (!comm) return fail(IABN_ERR_INVALID_ARG, "comm is NULL");
     if (comm->nranks == 1 || (flags & IABN_EVAL))
         return iabn_forward(desc, x, z, gamma, beta, running_mean, running_var, save_mean,
@@ -2207,6 +2329,7 @@ iabn_status iabn_backward_sync(const iabn_desc* desc, const void* z, const void*
                                const float* save_var, float* dgamma, float* dbeta, float eps,
                                float slope, uint32_t flags, void* ws, size_t ws_bytes,
                                void* stream, iabn_comm comm) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     if (!comm) return fail(IABN_ERR_INVALID_ARG, "comm is NULL");
     if (comm->nranks == 1)
         return iabn_backward(desc, z, dz, dx, gamma, beta, save_mean, save_var, dgamma, dbeta,
@@ -2274,6 +2397,7 @@ iabn_status iabn_forward_sync_emulated(const iabn_desc* desc, int nranks, const 
                                        float* running_mean, float* running_var, float* save_mean,
                                        float* save_var, float momentum, float eps, float slope,
                                        uint32_t flags, void* ws, size_t ws_bytes, void* stream) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     Ctx c;
     Geom gl;
     IABN_TRY(emu_ctx(desc, nranks, ws, ws_bytes, stream, &c, &gl));
@@ -2300,6 +2424,7 @@ iabn_status iabn_backward_sync_emulated(const iabn_desc* desc, int nranks, const
                                         const float* save_var, float* dgamma, float* dbeta,
                                         float eps, float slope, uint32_t flags, void* ws,
                                         size_t ws_bytes, void* stream) {
+    if (act_of(flags)) return fail(IABN_ERR_UNSUPPORTED, "sigmoid / tanh: iabn_forward / iabn_backward only");
     (void)save_mean;
     Ctx c;
     Geom gl;

@@ -130,6 +130,16 @@ def _flags(gamma_mode: str, running_var_biased: bool = False, extra: int = 0) ->
     return _GAMMA[gamma_mode] | (L.RUNNING_VAR_BIASED if running_var_biased else 0) | extra
 
 
+# f after BN; sigmoid / tanh: fp32, iabn_forward / iabn_backward only
+ACTIVATIONS = {"leaky_relu": 0, "sigmoid": L.ACT_SIGMOID, "tanh": L.ACT_TANH}
+
+
+def _act(activation: str) -> int:
+    if activation not in ACTIVATIONS:
+        raise ValueError(f"activation must be one of {sorted(ACTIVATIONS)}, got {activation!r}")
+    return ACTIVATIONS[activation]
+
+
 def broadcast_unique_id(group, make_id) -> bytes:
     """Rank 0 of `group` calls make_id(); every rank returns rank 0's 128 bytes."""
     import torch.distributed as dist
@@ -193,8 +203,9 @@ def forward(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
             momentum: float = 0.1, eps: float = 1e-5, slope: float = 0.01,
             out: torch.Tensor | None = None, training: bool = True, gamma_mode: str = "abs_eps",
             running_var_biased: bool = False, layout: str = "NCHW", flags: int = 0,
-            comm: Comm | None = None, stream=None):
-    """Alg. 1: z = f(BN_{gamma,beta}(x)), written over x unless ``out`` is given.
+            comm: Comm | None = None, stream=None, activation: str = "leaky_relu"):
+    """Alg. 1: z = f(BN_{gamma,beta}(x)), written over x unless ``out`` is given; f is
+    leaky ReLU with ``slope`` (default), sigmoid or tanh (``activation``).
     Returns (z, save_mean, save_var); in eval mode save_* are None."""
     d = _desc(x, layout)
     C = d.c
@@ -204,7 +215,8 @@ def forward(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor,
     gamma, beta = _f32(gamma, C, "gamma"), _f32(beta, C, "beta")
     running_mean = _f32(running_mean, C, "running_mean")
     running_var = _f32(running_var, C, "running_var")
-    fl = _flags(gamma_mode, running_var_biased, flags) | (0 if training else L.EVAL)
+    fl = _flags(gamma_mode, running_var_biased, flags | _act(activation)) | \
+        (0 if training else L.EVAL)
     if training:
         save_mean = _empty_c(C, x.device, stream)
         save_var = _empty_c(C, x.device, stream)
@@ -225,7 +237,7 @@ def backward(z: torch.Tensor, dz: torch.Tensor, gamma: torch.Tensor, beta: torch
              save_var: torch.Tensor, *, save_mean: torch.Tensor | None = None, eps: float = 1e-5,
              slope: float = 0.01, dx: torch.Tensor | None = None, gamma_mode: str = "abs_eps",
              layout: str = "NCHW", flags: int = 0, comm: Comm | None = None,
-             global_param_grads: bool = False, stream=None):
+             global_param_grads: bool = False, stream=None, activation: str = "leaky_relu"):
     """Alg. 2: from z and dL/dz only (variant II / BN-dagger in the channel-resident
     kernels, I in the streaming ones and with IABN_VARIANT_I; R6).  dx is
     written over dz unless ``dx`` is given.  Returns (dx, dgamma, dbeta)."""
@@ -238,7 +250,8 @@ def backward(z: torch.Tensor, dz: torch.Tensor, gamma: torch.Tensor, beta: torch
     save_var = _f32(save_var, C, "save_var")
     dgamma = _empty_c(C, z.device, stream)
     dbeta = _empty_c(C, z.device, stream)
-    fl = _flags(gamma_mode, False, flags) | (L.SYNC_GLOBAL_PARAM_GRADS if global_param_grads else 0)
+    fl = _flags(gamma_mode, False, flags | _act(activation)) | \
+        (L.SYNC_GLOBAL_PARAM_GRADS if global_param_grads else 0)
     ws, nb = workspace(d, z.device, stream)
     args = [ctypes.byref(d), z.data_ptr(), dz.data_ptr(), dx.data_ptr(), gamma.data_ptr(),
             beta.data_ptr(), _ptr(save_mean), save_var.data_ptr(), dgamma.data_ptr(),
@@ -403,48 +416,56 @@ class InPlaceABNFunction(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, gamma, beta, running_mean, running_var, momentum, eps, slope, training,
-                gamma_mode, layout, comm, grad_inplace=True):
+                gamma_mode, layout, comm, grad_inplace=True, activation="leaky_relu"):
         z, _, save_var = forward(x, gamma.detach(), beta.detach(), running_mean, running_var,
                                  momentum=momentum, eps=eps, slope=slope, training=training,
-                                 gamma_mode=gamma_mode, layout=layout, comm=comm)
+                                 gamma_mode=gamma_mode, layout=layout, comm=comm,
+                                 activation=activation)
         ctx.mark_dirty(x)
         ctx.save_for_backward(z, gamma, beta, save_var)
-        ctx.cfg = (eps, slope, gamma_mode, layout, comm, training, grad_inplace)
+        ctx.cfg = (eps, slope, gamma_mode, layout, comm, training, grad_inplace, activation)
         return z
 
     @staticmethod
     def backward(ctx, dz):
         z, gamma, beta, save_var = ctx.saved_tensors
-        eps, slope, gamma_mode, layout, comm, training, grad_inplace = ctx.cfg
+        eps, slope, gamma_mode, layout, comm, training, grad_inplace, activation = ctx.cfg
         if not training:
             raise RuntimeError("backward through eval-mode InPlace-ABN is not supported")
         dz = dz.contiguous()
         # gradient sharing: dL/dx is written over dL/dz unless disabled
         dx, dgamma, dbeta = backward(z, dz, gamma.detach(), beta.detach(), save_var, eps=eps,
                                      slope=slope, dx=None if grad_inplace else torch.empty_like(dz),
-                                     gamma_mode=gamma_mode, layout=layout, comm=comm)
-        return dx, dgamma, dbeta, None, None, None, None, None, None, None, None, None, None
+                                     gamma_mode=gamma_mode, layout=layout, comm=comm,
+                                     activation=activation)
+        return (dx, dgamma, dbeta, None, None, None, None, None, None, None, None, None, None,
+                None)
 
 
 def inplace_abn(x, gamma, beta, running_mean=None, running_var=None, *, momentum=0.1, eps=1e-5,
                 slope=0.01, training=True, gamma_mode="abs_eps", layout="NCHW", comm=None,
-                grad_inplace=True):
+                grad_inplace=True, activation="leaky_relu"):
     """Autograd entry: z written over x (mark_dirty) and, with ``grad_inplace`` (default,
     the paper's gradient sharing), dL/dx written over the incoming dL/dz.
     The incoming gradient buffer is then consumed: pass ``grad_inplace=False`` if a
     caller keeps its own reference to the gradient it feeds in (e.g. z.backward(g) with
     a g it reuses)."""
     return InPlaceABNFunction.apply(x, gamma, beta, running_mean, running_var, momentum, eps,
-                                    slope, training, gamma_mode, layout, comm, grad_inplace)
+                                    slope, training, gamma_mode, layout, comm, grad_inplace,
+                                    activation)
 
 
 class InPlaceABN(torch.nn.Module):
-    """The plug-in BN+LeakyReLU layer of PAPER.md:200 (fp32 gamma/beta, running stats)."""
+    """The plug-in BN+LeakyReLU layer of PAPER.md:200 (fp32 gamma/beta, running stats);
+    ``activation`` = "sigmoid" / "tanh" for the other invertible activations of
+    PAPER.md:142 (fp32 activations, no comm)."""
 
     def __init__(self, num_features: int, *, eps=1e-5, momentum=0.1, slope=0.01,
                  gamma_mode="abs_eps", comm: Comm | None = None, device=None,
-                 grad_inplace: bool = True):
+                 grad_inplace: bool = True, activation: str = "leaky_relu"):
         super().__init__()
+        _act(activation)
+        self.activation = activation
         self.grad_inplace = grad_inplace
         self.weight = torch.nn.Parameter(torch.ones(num_features, device=device))
         self.bias = torch.nn.Parameter(torch.zeros(num_features, device=device))
@@ -459,5 +480,6 @@ class InPlaceABN(torch.nn.Module):
         z = inplace_abn(xs, self.weight, self.bias, self.running_mean, self.running_var,
                         momentum=self.momentum, eps=self.eps, slope=self.slope,
                         training=self.training, gamma_mode=self.gamma_mode, layout=layout,
-                        comm=self.comm, grad_inplace=self.grad_inplace)
+                        comm=self.comm, grad_inplace=self.grad_inplace,
+                        activation=self.activation)
         return z if layout == "NCHW" else z.permute(0, 3, 1, 2)

@@ -214,3 +214,28 @@ def test_build_entry_does_not_import_package_before_library_exists():
             "assert 'paper_1712_02616_b200' not in sys.modules;"
             "assert callable(m.build) and m.LIB.endswith('libiabn.so')")
     subprocess.run([sys.executable, "-c", code, root], check=True, cwd="/")
+
+
+# ---------------------------------------------------------------- sigmoid / tanh
+def test_activation_flag_validation():
+    f32, bf16 = L.desc(2, 8, 16, L.F32, L.NCHW), L.desc(2, 8, 16, L.BF16, L.NHWC)
+    both = L.ACT_SIGMOID | L.ACT_TANH
+    assert _fwd(f32, flags=both) == L.ERR_INVALID_ARG
+    assert _bwd(f32, flags=both) == L.ERR_INVALID_ARG
+    for act in (L.ACT_SIGMOID, L.ACT_TANH):
+        assert _fwd(bf16, flags=act) == L.ERR_UNSUPPORTED  # fp32 storage only
+        assert _bwd(bf16, flags=act) == L.ERR_UNSUPPORTED
+        assert _fwd_emu(f32, 2, flags=act) == L.ERR_UNSUPPORTED  # single-GPU entries only
+        assert L.lib.iabn_forward_apply(ctypes.byref(f32), P, P, P, P, P, P, P, P, P, 0.1, 1e-5,
+                                        0.01, act, P * 16, L.workspace_bytes(f32),
+                                        None) == L.ERR_UNSUPPORTED
+
+
+def test_activation_names():
+    import paper_1712_02616_b200 as Pk
+    from paper_1712_02616_b200 import functional as F
+    assert F._act("leaky_relu") == 0 and F._act("sigmoid") == L.ACT_SIGMOID
+    with pytest.raises(ValueError):
+        F._act("relu")  # not invertible
+    with pytest.raises(ValueError):
+        Pk.InPlaceABN(4, activation="gelu")
