@@ -178,6 +178,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialisation may start while the previous kernel of the stream finishes; every
 // kernel calls this before its first global-memory access (read or write), which
@@ -279,6 +282,15 @@ __device__ __forceinline__ uint32_t cluster_nctarank() {
     return r;
 }
 // Read a double from the shared memory of CTA `rank` of this cluster (DSMEM).
+__device__ __forceinline__ long long ld_dsmem_s64(const long long* local_ptr, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                 : "=r"(remote)
+                 : "r"((uint32_t)__cvta_generic_to_shared(local_ptr)), "r"(rank));
+    long long v;
+    asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(remote));
+    return v;
+}
 __device__ __forceinline__ double ld_dsmem_f64(const double* local_ptr, uint32_t rank) {
     uint32_t remote;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"

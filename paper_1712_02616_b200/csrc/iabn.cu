@@ -27,6 +27,7 @@
 #include "kernels_gres.cuh"
 #include "kernels_fused.cuh"
 #include "kernels_nhwc.cuh"
+#include "kernels_nhwc_bulk.cuh"
 #include "kernels_small.cuh"
 #include "kernels_stream.cuh"
 
@@ -113,6 +114,16 @@ iabn_status device_facts(DevFacts** out) {
                               (const void*)nhwc_fused_kernel<float, 1>,
                               (const void*)nhwc_fused_kernel<__nv_bfloat16, 1>};
         for (const void* fn : nhwc) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        const void* nb[] = {(const void*)nhwc_bulk_reduce_kernel<float, 0, false>,
+                            (const void*)nhwc_bulk_reduce_kernel<float, 1, false>,
+                            (const void*)nhwc_bulk_reduce_kernel<float, 1, true>,
+                            (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 0, false>,
+                            (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 1, false>,
+                            (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 1, true>};
+        for (const void* fn : nb) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNbSmem);
+            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        }
         const void* gres[] = {(const void*)gres_kernel<float, 0>,
                               (const void*)gres_kernel<__nv_bfloat16, 0>,
                               (const void*)gres_kernel<float, 1>,
@@ -174,7 +185,29 @@ bool vec_ok(const Geom& g) {
 #define IABN_TARGET_WAVES 1
 #endif
 constexpr int64_t kTargetCtas = 148 * 8 * IABN_TARGET_WAVES;
+// NHWC streaming reductions through the bulk ring (kernels_nhwc_bulk.cuh): 16-byte rows
+// of <= 512 vectors; CTAs own whole row ranges, at most 2 per SM of a 148-SM B200 (a
+// device constant: workspace sizes must not depend on the device), at least one 16 KB
+// stage each.  0 = not applicable.
+int env_int(const char* name, int dflt);
+int nb_grid(const Geom& g) {
+    if (g.layout != IABN_NHWC || !vec_ok(g) || env_int("IABN_NHWC_BULK", 1) == 0) return 0;
+    if (g.C * g.b > 4096) return 0;  // <= 256 vectors per row
+    const int64_t bytes = g.m * g.C * g.b;  // one input
+    // 32 clusters of 8: resident at once (2 CTAs per SM; cudaOccupancyMaxActiveClusters
+    // reports 33 on a 148-SM B200 -- 37 clusters ran a second wave of 4)
+    int64_t G = std::min<int64_t>(32 * kNbCluster, bytes / kNbStageBytes);
+    G = std::min<int64_t>(G, g.m) / kNbCluster * kNbCluster;  // whole clusters
+    return (int)(G / kNbCluster);  // records: one per cluster
+}
+
+int stat_splits_ldg(const Geom& g);
 int stat_splits(const Geom& g) {
+    if (const int G = nb_grid(g)) return G;
+    return stat_splits_ldg(g);
+}
+// splits of the LDG reduction kernels (the workspace holds max(S, 296) NHWC records)
+int stat_splits_ldg(const Geom& g) {
     const int64_t target = kTargetCtas;
     int64_t units, per_unit_min, work;
     if (g.layout == IABN_NCHW) {
@@ -1093,6 +1126,71 @@ iabn_status launch_gres(const Geom& g, int G, GresArgs a, cudaStream_t st) {
 }
 
 // ====================================================================== streaming launches
+template <typename T, int PASS>
+iabn_status launch_nb(const Geom& g, int S, const void* in0, const void* in1, const float* gamma,
+                      const float* beta, float eps, float slope, uint32_t flags, double* part,
+                      cudaStream_t st) {
+    NbArgs a{};
+    a.in0 = in0;
+    a.in1 = in1;
+    a.gamma = gamma;
+    a.beta = beta;
+    a.C = g.C;
+    a.rows = g.m;
+    a.cv = (uint32_t)(g.C * g.b / 16);
+    a.rt = std::max<uint32_t>(1, (uint32_t)kThreads / a.cv);
+    a.rps = std::max<uint32_t>(1, kNbStageBytes / (PASS == 0 ? 1 : 2) / (a.cv * 16));
+    a.eps = eps;
+    a.slope = slope;
+    a.flags = flags;
+    a.part = part;
+    a.trace = nullptr;
+    if (env_int("IABN_NB_TRACE", 0)) {  // experiments only: phase timestamps
+        static unsigned long long* buf = nullptr;
+        static size_t cap = 0;
+        const size_t need = (size_t)S * kNbCluster * kNbTrace;
+        if (need > cap) {
+            if (buf) cudaFree(buf);
+            cudaMalloc(&buf, need * sizeof(unsigned long long));
+            cap = need;
+        }
+        a.trace = buf;
+        g_trace = buf;
+        g_trace_n = need;
+        g_trace_ch = (uint32_t)kNbTrace;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(S * kNbCluster));
+    cfg.blockDim = dim3(a.rt * a.cv);
+    cfg.dynamicSmemBytes = kNbSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kNbCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    if (a.trace) {  // experiments: residency of this launch
+        int nc = -1, nb = -1;
+        cudaOccupancyMaxActiveClusters(&nc, (const void*)nhwc_bulk_reduce_kernel<T, PASS, false>, &cfg);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)nhwc_bulk_reduce_kernel<T, PASS, false>,
+                                                      (int)cfg.blockDim.x, kNbSmem);
+        fprintf(stderr, "nb: grid %u block %u smem %zu: max active clusters %d, blocks/SM %d\n",
+                cfg.gridDim.x, cfg.blockDim.x, (size_t)kNbSmem, nc, nb);
+        cudaGetLastError();
+    }
+    if (PASS == 0)
+        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 0, false>, a);
+    else if (flags & IABN_VARIANT_I)
+        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 1, false>, a);
+    else
+        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 1, true>, a);
+    return check_launch(PASS == 0 ? "nhwc_bulk_reduce<stats>" : "nhwc_bulk_reduce<grad>");
+}
+
 template <typename T>
 iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cudaStream_t st) {
     const bool vec = vec_ok(g);
@@ -1106,6 +1204,8 @@ iabn_status launch_stats(const Geom& g, int S, const void* x, double* part, cuda
             launch_pdl(nchw_cover_kernel<T, 0>, grid, kThreads, 0, st,
                 (const T*)x, nullptr, nullptr, nullptr, g.C, g.HW, g.N, g.E, 0.f, 1.f, 1.f, 0u,
                 cover_fd(g), part);
+    } else if (nb_grid(g)) {
+        return launch_nb<T, 0>(g, S, x, nullptr, nullptr, nullptr, 1e-5f, 1.f, 0u, part, st);
     } else {
         const int V = vec ? 16 / g.b : 1;
         const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
@@ -1134,6 +1234,8 @@ iabn_status launch_bwd_reduce(const Geom& g, int S, const void* z, const void* d
             launch_pdl(nchw_cover_kernel<T, 1>, grid, kThreads, 0, st,
                 (const T*)z, (const T*)dz, gamma, beta, g.C, g.HW, g.N, g.E, eps, slope,
                 inv_slope, flags, cover_fd(g), part);
+    } else if (nb_grid(g)) {
+        return launch_nb<T, 1>(g, S, z, dz, gamma, beta, eps, slope, flags, part, st);
     } else {
         const int V = vec ? 16 / g.b : 1;
         const dim3 grid((unsigned)((g.C + 16 * V - 1) / (16 * V)), (unsigned)S);
@@ -1171,8 +1273,10 @@ int apply_grid(int64_t E, int b, int sms) {
 int nhwc_grid(const Geom& g, int64_t nvec, int sms) {
     const int64_t cv = g.C * g.b / 16;
     const int64_t q = cv / std::gcd<int64_t>(cv, kThreads);  // grid must be a multiple of q
-    const int64_t want = std::min<int64_t>((nvec + kThreads * kUnroll - 1) / (kThreads * kUnroll),
-                                           (int64_t)sms * 8);
+    // one batch of kNhwcApplyUnroll vectors per thread (later waves of CTAs start as earlier ones
+    // finish; r02: a cap of 8 CTAs per SM left threads a dependent tail)
+    const int64_t want = std::min<int64_t>((nvec + kThreads * kNhwcApplyUnroll - 1) / (kThreads * kNhwcApplyUnroll),
+                                           (int64_t)sms * 64);
     if (q > (int64_t)sms * 16) return 0;
     return (int)(std::max<int64_t>(1, (want + q - 1) / q) * q);
 }
@@ -1752,9 +1856,11 @@ iabn_status act_backward(const Ctx& c, const float* z, const float* dz, float* d
     double* part = wsp<double>(c, c.w.part);
     float4* coef = wsp<float4>(c, c.w.coef);
     const bool sig = flags & IABN_ACT_SIGMOID;
-    IABN_TRY(sig ? act_reduce<1>(c.g, c.S, z, dz, gamma, beta, eps, flags, part, c.st)
-                 : act_reduce<2>(c.g, c.S, z, dz, gamma, beta, eps, flags, part, c.st));
-    BwdCoefArgs a{part, c.S, part, c.S, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg, db,
+    // NHWC: the LDG splits (c.S may count bulk-ring clusters), within the workspace's 296
+    const int S = c.g.layout == IABN_NHWC ? (int)std::min<int64_t>(stat_splits_ldg(c.g), kGresMaxG) : c.S;
+    IABN_TRY(sig ? act_reduce<1>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st)
+                 : act_reduce<2>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st));
+    BwdCoefArgs a{part, S, part, S, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg, db,
                   coef, eps, flags};
     launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
     IABN_TRY(check_launch("bwd_coef kernel"));

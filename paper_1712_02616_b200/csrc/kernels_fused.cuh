@@ -243,9 +243,6 @@ constexpr int kApplyWarp0 = IABN_WARP_ORDER ? 2 : kReduceWarps;
 constexpr int kReduceWarp0 = IABN_WARP_ORDER ? 2 + kApplyWarps : 0;
 constexpr int kFusedThreads = (kWorkerWarps + 2) * 32;
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
 // named barrier over a worker group (id 1: reduce warps, 2: apply warps)
 __device__ __forceinline__ void group_sync(uint32_t id, uint32_t nthr) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");

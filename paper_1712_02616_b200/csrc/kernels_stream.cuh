@@ -45,6 +45,12 @@ constexpr int kStatUnroll = IABN_STAT_UNROLL;  // statistics kernel (one input)
 #define IABN_NHWC_UNROLL 4
 #endif
 constexpr int kNhwcUnroll = IABN_NHWC_UNROLL;  // NHWC reductions: rows in flight per thread
+#ifndef IABN_NHWC_APPLY_UNROLL
+#define IABN_NHWC_APPLY_UNROLL 8
+#endif
+// NHWC apply kernels: vectors in flight per thread (their register count caps the CTAs
+// per SM at 3-4, so the bytes in flight come from the depth per thread)
+constexpr int kNhwcApplyUnroll = IABN_NHWC_APPLY_UNROLL;
 
 // Gamma reparametrisation (R4).
 enum : uint32_t {
@@ -1244,6 +1250,10 @@ __global__ void __launch_bounds__(kThreads)
 // host sizes the grid so that the grid stride (gridDim.x*kThreads vectors) is a
 // multiple of C/V: every thread then keeps ONE channel group for the whole walk,
 // its V channels' coefficients live in registers, and the loop is pure streaming.
+// Per thread: batches of kNhwcApplyUnroll vectors (stride apart), every load of a batch predicated
+// and in flight before its math; the first batch is issued before the coefficient loads
+// so that the two latencies overlap, and the host sizes the grid so that most threads
+// run one batch (r02: a tail of single dependent loads cost 1-2 extra latencies).
 template <typename T>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_nhwc_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
@@ -1254,6 +1264,13 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t stride = gridDim.x * kThreads;
     uint32_t v = blockIdx.x * kThreads + threadIdx.x;
     if (v >= nvec) return;
+    uint4 r[kNhwcApplyUnroll];
+    auto load = [&](uint32_t vb) {
+#pragma unroll
+        for (int u = 0; u < kNhwcApplyUnroll; ++u)
+            if (vb + u * stride < nvec) r[u] = ld_vec(x + (size_t)(vb + u * stride) * V);
+    };
+    load(v);
     const uint32_t c0 = (v % cv) * V;
     float2 A[NP], B[NP], M[NP];  // per channel pair: A, beta - mu_lo A, mu_hi
 #pragma unroll
@@ -1264,9 +1281,9 @@ __global__ void __launch_bounds__(kThreads)
         M[i] = make_float2(c_a.y, c_b.y);
     }
     const float2 sl2 = make_float2(slope, slope);
-    auto apply = [&](const uint4 r, const uint32_t vv) {
+    auto apply = [&](const uint4 rr, const uint32_t vv) {
         float2 w[NP];
-        Pairs<T>::load(r, w);
+        Pairs<T>::load(rr, w);
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
             const float2 y = fma2(add2(w[i], make_float2(-M[i].x, -M[i].y)), A[i], B[i]);
@@ -1275,14 +1292,14 @@ __global__ void __launch_bounds__(kThreads)
         }
         st_vec(z + (size_t)vv * V, Pairs<T>::store(w));
     };
-    for (; v + (kUnroll - 1) * stride < nvec; v += kUnroll * stride) {
-        uint4 r[kUnroll];
+    while (true) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) r[u] = ld_vec(x + (size_t)(v + u * stride) * V);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) apply(r[u], v + u * stride);
+        for (int u = 0; u < kNhwcApplyUnroll; ++u)
+            if (v + u * stride < nvec) apply(r[u], v + u * stride);
+        v += kNhwcApplyUnroll * stride;
+        if (v >= nvec) break;
+        load(v);
     }
-    for (; v < nvec; v += stride) apply(ld_vec(x + (size_t)v * V), v);
 }
 
 template <typename T>
@@ -1295,6 +1312,16 @@ __global__ void __launch_bounds__(kThreads)
     const uint32_t stride = gridDim.x * kThreads;
     uint32_t v = blockIdx.x * kThreads + threadIdx.x;
     if (v >= nvec) return;
+    uint4 rz[kNhwcApplyUnroll], rd[kNhwcApplyUnroll];
+    auto load = [&](uint32_t vb) {
+#pragma unroll
+        for (int u = 0; u < kNhwcApplyUnroll; ++u)
+            if (vb + u * stride < nvec) {
+                rz[u] = ld_vec(z + (size_t)(vb + u * stride) * V);
+                rd[u] = ld_vec(dz + (size_t)(vb + u * stride) * V);
+            }
+    };
+    load(v);
     const uint32_t c0 = (v % cv) * V;
     float al[V], ka[V], cc[V];  // dx = al dy + ka y + cc
 #pragma unroll
@@ -1304,10 +1331,10 @@ __global__ void __launch_bounds__(kThreads)
         ka[k] = cf.y;
         cc[k] = cf.z;
     }
-    auto apply = [&](const uint4 rz, const uint4 rd, const uint32_t vv) {
+    auto apply = [&](const uint4 qz, const uint4 qd, const uint32_t vv) {
         float fz[V], fd[V];
-        unpack<T>(rz, fz);
-        unpack<T>(rd, fd);
+        unpack<T>(qz, fz);
+        unpack<T>(qd, fd);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             const bool pos = fz[k] >= 0.f;  // -0.0 counts as >= 0
@@ -1317,17 +1344,14 @@ __global__ void __launch_bounds__(kThreads)
         }
         st_vec(dx + (size_t)vv * V, pack<T>(fz));
     };
-    for (; v + (kUnroll - 1) * stride < nvec; v += kUnroll * stride) {
-        uint4 rz[kUnroll], rd[kUnroll];
+    while (true) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            rz[u] = ld_vec(z + (size_t)(v + u * stride) * V);
-            rd[u] = ld_vec(dz + (size_t)(v + u * stride) * V);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) apply(rz[u], rd[u], v + u * stride);
+        for (int u = 0; u < kNhwcApplyUnroll; ++u)
+            if (v + u * stride < nvec) apply(rz[u], rd[u], v + u * stride);
+        v += kNhwcApplyUnroll * stride;
+        if (v >= nvec) break;
+        load(v);
     }
-    for (; v < nvec; v += stride) apply(ld_vec(z + (size_t)v * V), ld_vec(dz + (size_t)v * V), v);
 }
 
 // ====================================================================== test-time folding

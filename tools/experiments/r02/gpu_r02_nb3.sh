@@ -1,0 +1,8 @@
+# NHWC streaming: bulk-ring reductions + deeper apply; tests, phase times, NHWC sweeps
+python -m pytest tests -m gpu -x -q > gpurun_out/nb_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/nb_tests.log
+tail -2 gpurun_out/nb_tests.log
+python tools/phase_time.py --shape 32x128x3136
+for net in densenet264 rx101; do for dt in bf16 f32; do
+  python tools/sweep.py --net $net --dtype $dt --layout NHWC > gpurun_out/nb_sweep_${net}_${dt}_on.json 2>&1
+  python -c "import json; d=json.loads(open('gpurun_out/nb_sweep_${net}_${dt}_on.json').read().strip().splitlines()[-1]); print('$net $dt', d['graph_ms'], d['graph_pct_of_peak'])"
+done; done
