@@ -2122,6 +2122,12 @@ IABN_API void iabn_debug_fault(uint32_t mask) { g_fault.store(mask); }
 // Test hook only (not in include/iabn.h): the register-resident small-layer schedule --
 // 1 = whenever the shape allows it (ignoring the size threshold), -1 = never, 0 = automatic.
 IABN_API void iabn_debug_small(int on) { g_small_force.store(on); }
+// test hook: record count of the NHWC bulk-ring reductions for this shape (0 = LDG kernels)
+IABN_API int iabn_debug_nb_records(const iabn_desc* desc) {
+    Geom g;
+    if (make_geom(desc, &g) != IABN_OK) return -1;
+    return nb_grid(g);
+}
 // ... and its slots per thread (4 or 8; 0 = automatic)
 IABN_API void iabn_debug_small_r(int r) { g_small_force_r.store(r); }
 
