@@ -939,6 +939,21 @@ iabn_status launch_small(int pass, const Geom& g, const SmallPlan& p, SmallArgs 
     a.W = p.W;
     a.fd_w = fd32(p.W);
     a.tw = p.tw;
+    a.trace = nullptr;
+    if (env_int("IABN_SMALL_TRACE", 0)) {  // experiments (a build with -DIABN_PHASE_TRACE)
+        static unsigned long long* buf = nullptr;
+        static size_t cap = 0;
+        const size_t need = (size_t)p.grid * kSmallTrace;
+        if (need > cap) {
+            if (buf) cudaFree(buf);
+            cudaMalloc(&buf, need * sizeof(unsigned long long));
+            cap = need;
+        }
+        a.trace = buf;
+        g_trace = buf;
+        g_trace_n = need;
+        g_trace_ch = (uint32_t)kSmallTrace;
+    }
     if (p.R == 4) {
         if (pass == 0) launch_pdl(small_kernel<T, 0, 4>, p.grid, kSmallThreads, 0, st, a);
         else launch_pdl(small_kernel<T, 1, 4>, p.grid, kSmallThreads, 0, st, a);

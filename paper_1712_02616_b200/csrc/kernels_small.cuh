@@ -48,7 +48,11 @@ struct SmallArgs {
     uint32_t tw;      // warps per channel team
     float momentum, eps, slope, inv_slope;
     uint32_t flags;
+    unsigned long long* trace;  // experiments: [grid][kSmallTrace] %globaltimer of CTA phases
 };
+// phases: 0 start, 1 PDL wait done, 2 thread 0's sums done (its loads landed), 3 team
+// partials in shared memory, 4 coefficients ready, 5 stores issued
+constexpr int kSmallTrace = 6;
 
 // element k of 16-byte slot i lies in the plane's bytes [h, h + hwb)
 template <typename T>
@@ -83,8 +87,20 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
     const uint32_t nslots = a.N * a.W;
     const char* in0 = static_cast<const char*>(a.in0);
     const char* in1 = static_cast<const char*>(a.in1);
-
+    auto trace = [&](int k) {
+#ifdef IABN_PHASE_TRACE  // experiments build only: the pointer costs registers (spills)
+        if (a.trace && tid == 0) {
+            unsigned long long tm;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+            a.trace[(size_t)blockIdx.x * kSmallTrace + k] = tm;
+        }
+#else
+        (void)k;
+#endif
+    };
+    trace(0);
     pdl_wait();
+    trace(1);
     // slot k of this thread: plane n = i / W, slot si = i % W of the plane's covering
     // range (recomputed where needed: registers go to the data)
     struct Slot {
@@ -154,6 +170,7 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
             }
         }
     }
+    trace(2);
     float r1 = PASS == 0 ? s1 : fmaf(-(1.f - a.slope), s2, s1);
     float r2 = PASS == 0 ? s2 : s3;
 #pragma unroll
@@ -166,6 +183,7 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
         red[warp][1] = r2;
     }
     __syncthreads();
+    trace(3);
     // ---- team leader: channel totals and coefficients
     if (tt == 0 && active) {
         double t1 = 0.0, t2 = 0.0;
@@ -202,6 +220,7 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
         }
     }
     __syncthreads();
+    trace(4);
     if (!active) return;
     // ---- outputs from the registers
     const float* co = cf[team];
@@ -237,6 +256,7 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
                     st_scalar<T>(dst + e, (e & 1) ? w[e >> 1].y : w[e >> 1].x);
         }
     }
+    trace(5);
 }
 
 }  // namespace iabn
