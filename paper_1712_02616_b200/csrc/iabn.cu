@@ -895,7 +895,7 @@ struct SmallPlan {
 std::atomic<int> g_small_force{0};  // test hook: 1 on when possible, -1 off, 0 automatic
 std::atomic<int> g_small_force_r{0};  // test hook: slots per thread (4 or 8), 0 automatic
 
-SmallPlan small_plan(const Geom& g, uint32_t flags) {
+SmallPlan small_plan(const Geom& g, uint32_t flags, int sms) {
     SmallPlan p;
     if (g.layout != IABN_NCHW || (flags & IABN_EVAL)) return p;
     const int f = g_small_force.load();
@@ -904,7 +904,11 @@ SmallPlan small_plan(const Geom& g, uint32_t flags) {
     // measured (tools/small_tune.py, profiles/r02_small_tune_*.log): faster than the
     // channel-resident kernels up to 16 KB per channel (bf16 14x14 and every 7x7 layer at
     // N = 32: -25..-42 % per pass); at 25 KB (fp32 14x14) equal or slower
-    if (!f && g.m * g.b > (int64_t)env_int("IABN_SMALL_MAX_KB", 16) * 1024) return p;
+    // Above 16 KB only when the layer is one wave at the R = 8 kernels' occupancy (2 CTAs
+    // per SM): fp32 128x14^2 (25 KB) 7.9 / 7.5 -> 5.4 / 5.4 us, while 512x14^2 (4 waves
+    // of channels) stays channel-resident (11.0 / 11.2 vs 11.8 / 12.3 us).
+    const bool one_wave = g.m * g.b <= 32 * 1024 && g.C <= 2 * (int64_t)sms;
+    if (!f && g.m * g.b > (int64_t)env_int("IABN_SMALL_MAX_KB", 16) * 1024 && !one_wave) return p;
     const int64_t W = (g.HW * g.b + 30) / 16;  // >= the slots covering any plane
     auto fit = [&](uint32_t R, SmallPlan& q) {
         for (uint32_t tw : {1u, 2u, 4u, 8u}) {
@@ -1898,7 +1902,7 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
     }
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
-        const SmallPlan sp = small_plan(c.g, flags);
+        const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
         if (sp.ok) {
             SmallArgs a{};
             a.in0 = x;
@@ -1989,7 +1993,7 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
             return act_backward(c, (const float*)z, (const float*)dz, (float*)dx, gamma, beta, sv,
                                 dg, db, eps, flags);
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
-        const SmallPlan sp = small_plan(c.g, flags);
+        const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
         if (sp.ok) {
             SmallArgs a{};
             a.in0 = z;
@@ -2179,7 +2183,7 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
         return IABN_OK;
     }
     if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
-        const SmallPlan sp = small_plan(g, flags);
+        const SmallPlan sp = small_plan(g, flags, dev->sms);
         if (sp.ok) {
             *schedule = 5;
             *cluster = 0;

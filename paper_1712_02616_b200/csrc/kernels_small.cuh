@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
     constexpr uint32_t B = sizeof(T);
     __shared__ double red[kSmallThreads / 32][2];
     __shared__ float cf[kSmallThreads / 32][8];
+    __shared__ double stash[kSmallThreads / 32][2];
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t tw = a.tw, TT = 32 * tw, team = warp / tw, tt = tid - team * TT;
@@ -200,9 +201,8 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
             co[0] = f.x;
             co[1] = f.y;
             co[2] = fmaf(-f.z, f.x, f.w);
-            a.save_mean[c] = (float)mean;
-            a.save_var[c] = (float)var;
-            update_running(a.running_mean, a.running_var, c, mean, var, n, a.momentum, a.flags);
+            stash[team][0] = mean;  // the global writes wait until after the barrier
+            stash[team][1] = var;
         } else {
             const double gg = gamma_eff(gam, a.eps, a.flags), bb = (double)bet;
             double S1 = t1, S2 = t2;
@@ -215,13 +215,28 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2
             co[2] = alpha * a.slope;
             co[3] = kappa * a.inv_slope;
             co[4] = (float)(rm * fma(S2, bb, -gg * S1));
-            a.dbeta[c] = (float)S1;
-            a.dgamma[c] = (float)(gamma_sign(gam, a.flags) * S2);
+            stash[team][0] = S1;
+            stash[team][1] = S2;
         }
     }
     __syncthreads();
     trace(4);
     if (!active) return;
+    // the leader's global writes (statistics, running update, parameter gradients) off the
+    // critical path: the team's stores below need only the coefficients (r02 phase trace:
+    // the running update's read-modify-write cost ~0.5 us before the barrier)
+    if (tt == 0) {
+        if (PASS == 0) {
+            const double mean = stash[team][0], var = stash[team][1];
+            a.save_mean[c] = (float)mean;
+            a.save_var[c] = (float)var;
+            update_running(a.running_mean, a.running_var, c, mean, var,
+                           (double)a.N * (double)a.HW, a.momentum, a.flags);
+        } else {
+            a.dbeta[c] = (float)stash[team][0];
+            a.dgamma[c] = (float)(gamma_sign(gam, a.flags) * stash[team][1]);
+        }
+    }
     // ---- outputs from the registers
     const float* co = cf[team];
     const float c0 = co[0], c1 = co[1], c2 = co[2], c3 = PASS == 1 ? co[3] : 0.f,
