@@ -27,6 +27,9 @@
 namespace iabn {
 
 constexpr int kSmallThreads = 256;
+#ifndef IABN_SMALL_MINB_F4
+#define IABN_SMALL_MINB_F4 4  // forward, R = 4: CTAs per SM the register cap is sized for
+#endif
 constexpr int kSmallR = 8;  // most 16-byte slots per thread and input (R = 4 or 8)
 
 struct SmallArgs {
@@ -70,7 +73,7 @@ __device__ __forceinline__ uint4 ldg_coherent(const void* p) {
 }
 
 template <typename T, int PASS, int R>
-__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? 4 : (PASS == 0 ? 3 : 2))
+__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMALL_MINB_F4 : 4) : (PASS == 0 ? 3 : 2))
     small_kernel(const SmallArgs a) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
