@@ -1300,9 +1300,9 @@ int nhwc_grid(const Geom& g, int64_t nvec, int sms) {
     return (int)(std::max<int64_t>(1, (want + q - 1) / q) * q);
 }
 
-template <typename T>
-iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4* coef,
-                             float slope, int sms, cudaStream_t st) {
+template <typename T, bool EV>
+iabn_status launch_fwd_apply_ev(const Geom& g, const void* x, void* z, const float4* coef,
+                                float slope, int sms, cudaStream_t st, const EvalCoef& ev) {
     const int64_t spc = samples_per_chunk(g);
     if (spc <= 0) return fail(IABN_ERR_UNSUPPORTED, "sample too large for the streaming apply");
     const bool al = vec_ok(g);
@@ -1315,25 +1315,30 @@ iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4
         T* zp = (T*)z + off;
         const int grid = apply_grid(E, g.b, sms);
         if (g.layout == IABN_NCHW && g.HW >= 16 / g.b) {  // any alignment (straddles handled)
-            launch_pdl(fwd_apply_rows_kernel<T>, grid, kThreads, 0, st,
-                xp, zp, coef, E, (uint32_t)g.HW, (uint32_t)g.C, fh, fc, slope);
+            launch_pdl(fwd_apply_rows_kernel<T, EV>, grid, kThreads, 0, st,
+                xp, zp, coef, E, (uint32_t)g.HW, (uint32_t)g.C, fh, fc, slope, ev);
         } else if (g.layout == IABN_NCHW) {
             if (al)
-                launch_pdl(fwd_apply_kernel<T, 0, true>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 0, true, EV>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope, ev);
             else
-                launch_pdl(fwd_apply_kernel<T, 0, false>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 0, false, EV>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope, ev);
         } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
-            launch_pdl(fwd_apply_nhwc_kernel<T>, nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st,
-                xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope);
+            launch_pdl(fwd_apply_nhwc_kernel<T, EV>, nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st,
+                xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope, ev);
         } else {
             if (al)
-                launch_pdl(fwd_apply_kernel<T, 1, true>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 1, true, EV>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope, ev);
             else
-                launch_pdl(fwd_apply_kernel<T, 1, false>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope);
+                launch_pdl(fwd_apply_kernel<T, 1, false, EV>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope, ev);
         }
         IABN_TRY(check_launch("fwd_apply kernel"));
     }
     return IABN_OK;
+}
+template <typename T>
+iabn_status launch_fwd_apply(const Geom& g, const void* x, void* z, const float4* coef,
+                             float slope, int sms, cudaStream_t st) {
+    return launch_fwd_apply_ev<T, false>(g, x, z, coef, slope, sms, st, EvalCoef{});
 }
 
 template <typename T>
@@ -1895,12 +1900,9 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
         if (act_of(flags))
             return act_forward(c, (const float*)x, (float*)z, gamma, beta, rm, rv, sm, sv,
                                momentum, eps, flags);
-    if (flags & IABN_EVAL) {
-        launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv, eps, flags,
-                                                         wsp<float4>(c, c.w.coef));
-        IABN_TRY(check_launch("eval_coef kernel"));
-        return launch_fwd_apply<T>(c.g, x, z, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
-    }
+    if (flags & IABN_EVAL)  // one launch: the apply derives its coefficients (EvalCoef)
+        return launch_fwd_apply_ev<T, true>(c.g, x, z, nullptr, slope, c.dev->sms, c.st,
+                                             EvalCoef{gamma, beta, rm, rv, eps, flags});
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
         const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
         if (sp.ok) {

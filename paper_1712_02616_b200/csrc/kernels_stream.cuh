@@ -481,6 +481,30 @@ __global__ void eval_coef_kernel(int64_t C, const float* __restrict__ gamma,
     coef[c] = make_float4((float)A, rm[c], 0.f, beta[c]);
 }
 
+// Eval forward without a coefficient launch: the apply kernels derive (A, mu, 0, beta)
+// per channel from the running statistics themselves (fp32: A = g~ rsqrt(r_var + eps),
+// within a few ulp of eval_coef_kernel's fp64 value).  r02: the extra launch cost
+// 1-3 us per layer (32x512x14^2 bf16 eval forward 6.9 -> 5.8 us, NHWC 32x128x56^2
+// 13.4 -> 10.2 us; a torch copy of the same tensors: 4.1 / 9.8 us).
+struct EvalCoef {
+    const float* gamma;
+    const float* beta;
+    const float* rm;
+    const float* rv;
+    float eps;
+    uint32_t flags;
+};
+template <bool NC, bool EV>
+__device__ __forceinline__ float4 get_coef(const float4* coef, const EvalCoef& ev, uint32_t c) {
+    if constexpr (EV) {
+        const float gm = __ldg(ev.gamma + c);
+        const float g = (ev.flags & kGammaFixedOne) ? 1.f : (ev.flags & kGammaPlain) ? gm : fabsf(gm) + ev.eps;
+        return make_float4(g * rsqrtf(__ldg(ev.rv + c) + ev.eps), __ldg(ev.rm + c), 0.f, __ldg(ev.beta + c));
+    } else {
+        return ld_coef<NC>(coef + c);
+    }
+}
+
 // ====================================================================== elementwise passes
 // Channel of flat element e (e < 2^32 within one launch; the host splits the
 // tensor into whole-sample chunks).
@@ -501,10 +525,10 @@ __device__ __forceinline__ float leaky(float y, float slope) { return y >= 0.f ?
 // multiple of 16 (a 16-byte vector lies in one channel) or NHWC with C*b a
 // multiple of 16 (a vector holds channels c0 .. c0+V-1); otherwise the channel
 // is resolved per element.
-template <typename T, int LAYOUT, bool ALIGNED, bool NC = true>
+template <typename T, int LAYOUT, bool ALIGNED, bool NC = true, bool EV = false>
 __device__ __forceinline__ void fwd_apply_body(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
                      FastDiv fd_c, float slope,
-        const Blk bk) {
+        const Blk bk, const EvalCoef& ev = EvalCoef{}) {
     constexpr int V = Elem<T>::kVec;
     const uint32_t nvec = E / V;
     const uint32_t stride = bk.nx * kThreads;
@@ -524,17 +548,17 @@ __device__ __forceinline__ void fwd_apply_body(const T* x, T* z, const float4* _
                 unpack<T>(r[u], f);
                 const uint32_t e = v * V;
                 if (ALIGNED && LAYOUT == 0) {  // NCHW: the vector lies in one channel
-                    const float4 cf = ld_coef<NC>(coef + channel_of<LAYOUT>(e, fd_hw, fd_c));
+                    const float4 cf = get_coef<NC, EV>(coef, ev, channel_of<LAYOUT>(e, fd_hw, fd_c));
 #pragma unroll
                     for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], cf), slope);
                 } else if (ALIGNED) {  // NHWC, C % V == 0: channels c0 .. c0+V-1
                     const uint32_t c0 = channel_of<LAYOUT>(e, fd_hw, fd_c);
 #pragma unroll
-                    for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], ld_coef<NC>(coef + c0 + k)), slope);
+                    for (int k = 0; k < V; ++k) f[k] = leaky(affine(f[k], get_coef<NC, EV>(coef, ev, c0 + k)), slope);
                 } else {
 #pragma unroll
                     for (int k = 0; k < V; ++k) {
-                        const float4 cf = ld_coef<NC>(coef + channel_of<LAYOUT>(e + k, fd_hw, fd_c));
+                        const float4 cf = get_coef<NC, EV>(coef, ev, channel_of<LAYOUT>(e + k, fd_hw, fd_c));
                         f[k] = leaky(affine(f[k], cf), slope);
                     }
                 }
@@ -545,16 +569,16 @@ __device__ __forceinline__ void fwd_apply_body(const T* x, T* z, const float4* _
     // tail (E % V elements) by the first threads of block 0
     if (bk.x == 0 && threadIdx.x < E - nvec * V) {
         const uint32_t e = nvec * V + threadIdx.x;
-        const float4 cf = coef[channel_of<LAYOUT>(e, fd_hw, fd_c)];
+        const float4 cf = get_coef<false, EV>(coef, ev, channel_of<LAYOUT>(e, fd_hw, fd_c));
         st_scalar<T>(z + e, leaky(affine(ld_scalar<T>(x + e), cf), slope));
     }
 }
-template <typename T, int LAYOUT, bool ALIGNED>
+template <typename T, int LAYOUT, bool ALIGNED, bool EV = false>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E, FastDiv fd_hw,
-                     FastDiv fd_c, float slope) {
+                     FastDiv fd_c, float slope, EvalCoef ev) {
     pdl_wait();
-    fwd_apply_body<T, LAYOUT, ALIGNED>(x, z, coef, E, fd_hw, fd_c, slope, hw_blk());
+    fwd_apply_body<T, LAYOUT, ALIGNED, true, EV>(x, z, coef, E, fd_hw, fd_c, slope, hw_blk(), ev);
 }
 
 
@@ -564,11 +588,11 @@ __global__ void __launch_bounds__(kThreads)
 // kUnroll loads issued before the math.  A vector that straddles two planes (HW*b
 // not a multiple of 16) takes its tail elements' coefficients from the next channel.
 // y = (x - mu_hi) A + (beta - mu_lo A), z = max(y, a y).
-template <typename T, bool NC = true>
+template <typename T, bool NC = true, bool EV = false>
 __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const float4* __restrict__ coef,
                                                     uint32_t E, uint32_t HW, uint32_t C,
                                                     FastDiv fd_hw, FastDiv fd_c, float slope,
-                                                    const Blk bk) {
+                                                    const Blk bk, const EvalCoef& ev = EvalCoef{}) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
     const uint32_t nvec = E / V;
@@ -576,7 +600,7 @@ __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const floa
     uint32_t v = bk.x * kThreads + threadIdx.x;
     if (bk.x == 0 && threadIdx.x < E - nvec * V) {  // tail elements
         const uint32_t e = nvec * V + threadIdx.x;
-        const float4 cf = ld_coef<NC>(coef + channel_of<0>(e, fd_hw, fd_c));
+        const float4 cf = get_coef<NC, EV>(coef, ev, channel_of<0>(e, fd_hw, fd_c));
         st_scalar<T>(z + e, leaky(affine(ld_scalar<T>(x + e), cf), slope));
     }
     if (v >= nvec) return;
@@ -589,7 +613,7 @@ __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const floa
     uint32_t c = row - fdiv(row, fd_c) * C;
     const float2 sl2 = make_float2(slope, slope);
     auto apply = [&](const uint4 r, const uint32_t cc, const uint32_t spv, const uint32_t vv) {
-        const float4 cf = ld_coef<NC>(coef + cc);  // (A, mu_hi, mu_lo, beta)
+        const float4 cf = get_coef<NC, EV>(coef, ev, cc);  // (A, mu_hi, mu_lo, beta)
         const float bp = fmaf(-cf.z, cf.x, cf.w);
         if (spv + V <= HW) {
             const float2 A2 = make_float2(cf.x, cf.x), B2 = make_float2(bp, bp);
@@ -603,7 +627,7 @@ __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const floa
             }
             st_vec(z + (size_t)vv * V, Pairs<T>::store(w));
         } else {  // elements k >= HW - spv belong to the next channel
-            const float4 cf2 = ld_coef<NC>(coef + (cc + 1 == C ? 0 : cc + 1));
+            const float4 cf2 = get_coef<NC, EV>(coef, ev, cc + 1 == C ? 0 : cc + 1);
             const float bp2 = fmaf(-cf2.z, cf2.x, cf2.w);
             const uint32_t kb = HW - spv;
             float f[V];
@@ -647,12 +671,13 @@ __device__ __forceinline__ void fwd_apply_rows_body(const T* x, T* z, const floa
         apply(r, cc, ss, vv);
     }
 }
-template <typename T>
+template <typename T, bool EV = false>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_rows_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t E,
-                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope) {
+                          uint32_t HW, uint32_t C, FastDiv fd_hw, FastDiv fd_c, float slope,
+                          EvalCoef ev) {
     pdl_wait();
-    fwd_apply_rows_body<T>(x, z, coef, E, HW, C, fd_hw, fd_c, slope, hw_blk());
+    fwd_apply_rows_body<T, true, EV>(x, z, coef, E, HW, C, fd_hw, fd_c, slope, hw_blk(), ev);
 }
 
 // ====================================================================== B1: gradient sums
@@ -1254,10 +1279,10 @@ __global__ void __launch_bounds__(kThreads)
 // and in flight before its math; the first batch is issued before the coefficient loads
 // so that the two latencies overlap, and the host sizes the grid so that most threads
 // run one batch (r02: a tail of single dependent loads cost 1-2 extra latencies).
-template <typename T>
+template <typename T, bool EV = false>
 __global__ void __launch_bounds__(kThreads)
     fwd_apply_nhwc_kernel(const T* x, T* z, const float4* __restrict__ coef, uint32_t nvec,
-                          uint32_t cv, float slope) {
+                          uint32_t cv, float slope, EvalCoef ev) {
     pdl_wait();
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = V / 2;
@@ -1275,7 +1300,8 @@ __global__ void __launch_bounds__(kThreads)
     float2 A[NP], B[NP], M[NP];  // per channel pair: A, beta - mu_lo A, mu_hi
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
-        const float4 c_a = __ldg(coef + c0 + 2 * i), c_b = __ldg(coef + c0 + 2 * i + 1);
+        const float4 c_a = get_coef<true, EV>(coef, ev, c0 + 2 * i),
+                     c_b = get_coef<true, EV>(coef, ev, c0 + 2 * i + 1);
         A[i] = make_float2(c_a.x, c_b.x);
         B[i] = make_float2(fmaf(-c_a.z, c_a.x, c_a.w), fmaf(-c_b.z, c_b.x, c_b.w));
         M[i] = make_float2(c_a.y, c_b.y);
