@@ -109,6 +109,18 @@ iabn_status device_facts(DevFacts** out) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
             cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         }
+        const void* act[] = {(const void*)fused_kernel<float, 0, 2, false, 1>, (const void*)fused_kernel<float, 1, 2, false, 1>,
+                             (const void*)fused_kernel<float, 0, 4, false, 1>, (const void*)fused_kernel<float, 1, 4, false, 1>,
+                             (const void*)fused_kernel<float, 0, 2, true, 1>, (const void*)fused_kernel<float, 1, 2, true, 1>,
+                             (const void*)fused_kernel<float, 0, 4, true, 1>, (const void*)fused_kernel<float, 1, 4, true, 1>,
+                             (const void*)fused_kernel<float, 0, 2, false, 2>, (const void*)fused_kernel<float, 1, 2, false, 2>,
+                             (const void*)fused_kernel<float, 0, 4, false, 2>, (const void*)fused_kernel<float, 1, 4, false, 2>,
+                             (const void*)fused_kernel<float, 0, 2, true, 2>, (const void*)fused_kernel<float, 1, 2, true, 2>,
+                             (const void*)fused_kernel<float, 0, 4, true, 2>, (const void*)fused_kernel<float, 1, 4, true, 2>};
+        for (const void* fn : act) {  // BN + sigmoid / tanh in the channel-resident kernels
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        }
         const void* nhwc[] = {(const void*)nhwc_fused_kernel<float, 0>,
                               (const void*)nhwc_fused_kernel<__nv_bfloat16, 0>,
                               (const void*)nhwc_fused_kernel<float, 1>,
@@ -592,7 +604,7 @@ unsigned int* dyn_counters(cudaStream_t st) {
     return p;
 }
 
-template <typename T>
+template <typename T, int ACT = 0>
 iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t st) {
     a.dyn = nullptr;
     if (a.qv == 0) {  // plain call: one rank, no exchange
@@ -698,17 +710,17 @@ iabn_status launch_fused(int pass, const FusedPlan& p, FusedArgs a, cudaStream_t
     a.fd_w = fd32(p.mis ? p.mis_w : 1);
     if (p.mis) {
         if (p.minb == 4)
-            e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4, true>, a)
-                          : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4, true>, a);
+            e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4, true, ACT>, a)
+                          : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4, true, ACT>, a);
         else
-            e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2, true>, a)
-                          : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2, true>, a);
+            e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2, true, ACT>, a)
+                          : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2, true, ACT>, a);
     } else if (p.minb == 4) {
-        e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4>, a)
-                      : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4>, a);
+        e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 4, false, ACT>, a)
+                      : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 4, false, ACT>, a);
     } else {
-        e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2>, a)
-                      : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2>, a);
+        e = pass == 0 ? cudaLaunchKernelEx(&cfg, fused_kernel<T, 0, 2, false, ACT>, a)
+                      : cudaLaunchKernelEx(&cfg, fused_kernel<T, 1, 2, false, ACT>, a);
     }
     if (e != cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1858,6 +1870,15 @@ iabn_status act_reduce(const Geom& g, int S, const float* z, const float* dz, co
 iabn_status act_forward(const Ctx& c, const float* x, float* z, const float* gamma,
                         const float* beta, float* rm, float* rv, float* sm, float* sv,
                         float momentum, float eps, uint32_t flags) {
+    if (!(flags & (IABN_EVAL | IABN_FORCE_STREAMING))) {  // NCHW: the channel-resident kernels
+        const FusedPlan p = fused_plan(c.g, 0, *c.dev, flags);
+        if (p.ok) {
+            const FusedArgs a = fused_fwd_args(c.g, x, z, gamma, beta, rm, rv, sm, sv, momentum,
+                                               eps, 1.f, flags);
+            return (flags & IABN_ACT_SIGMOID) ? launch_fused<float, 1>(0, p, a, c.st)
+                                              : launch_fused<float, 2>(0, p, a, c.st);
+        }
+    }
     float4* coef = wsp<float4>(c, c.w.coef);
     if (flags & IABN_EVAL) {
         launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv, eps, flags, coef);
@@ -1877,9 +1898,17 @@ iabn_status act_forward(const Ctx& c, const float* x, float* z, const float* gam
 iabn_status act_backward(const Ctx& c, const float* z, const float* dz, float* dx,
                          const float* gamma, const float* beta, const float* sv, float* dg,
                          float* db, float eps, uint32_t flags) {
+    const bool sig = flags & IABN_ACT_SIGMOID;
+    if (!(flags & IABN_FORCE_STREAMING)) {
+        const FusedPlan p = fused_plan(c.g, 1, *c.dev, flags);
+        if (p.ok) {
+            const FusedArgs a = fused_bwd_args(c.g, z, dz, dx, gamma, beta, sv, dg, db, eps, 1.f,
+                                               flags);
+            return sig ? launch_fused<float, 1>(1, p, a, c.st) : launch_fused<float, 2>(1, p, a, c.st);
+        }
+    }
     double* part = wsp<double>(c, c.w.part);
     float4* coef = wsp<float4>(c, c.w.coef);
-    const bool sig = flags & IABN_ACT_SIGMOID;
     // NHWC: the LDG splits (c.S may count bulk-ring clusters), within the workspace's 296
     const int S = c.g.layout == IABN_NHWC ? (int)std::min<int64_t>(stat_splits_ldg(c.g), kGresMaxG) : c.S;
     IABN_TRY(sig ? act_reduce<1>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st)
@@ -2178,10 +2207,12 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     if (pass != 0 && pass != 1) return fail(IABN_ERR_INVALID_ARG, "pass must be 0 or 1");
     DevFacts* dev;
     IABN_TRY(device_facts(&dev));
-    if (act_of(flags)) {  // sigmoid / tanh: streaming only
+    if (act_of(flags)) {  // sigmoid / tanh: channel-resident (NCHW) or streaming
         IABN_TRY(check_act_flags(g, flags));
-        *schedule = 0;
-        *cluster = 0;
+        FusedPlan p;
+        if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL))) p = fused_plan(g, pass, *dev, flags);
+        *schedule = p.ok ? 1 : 0;
+        *cluster = p.ok ? p.K : 0;
         return IABN_OK;
     }
     if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {

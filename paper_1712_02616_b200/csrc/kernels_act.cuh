@@ -34,8 +34,11 @@ constexpr float kOneBelow1 = 0.99999994f;  // 1 - 2^-24, the largest float below
 template <int ACT>  // 1 = sigmoid, 2 = tanh
 struct Act {
     static __device__ __forceinline__ float f(float y) {
-        if (ACT == 1) return __frcp_rn(1.f + __expf(-y));
-        return 1.f - 2.f * __frcp_rn(__expf(2.f * y) + 1.f);  // +-inf / 0 give +-1
+        // __fdividef: MUFU.RCP + one multiply (__frcp_rn is a correctly rounded software
+        // sequence: it made the channel-resident forward's apply warps ALU-bound); for a
+        // denominator beyond 2^126 (y < -87) the quotient is 0, the limit
+        if (ACT == 1) return __fdividef(1.f, 1.f + __expf(-y));
+        return 1.f - __fdividef(2.f, __expf(2.f * y) + 1.f);  // +-inf / 0 give +-1
     }
     static __device__ __forceinline__ float df(float z) {  // f'(f^-1(z))
         if (ACT == 1) return z * (1.f - z);

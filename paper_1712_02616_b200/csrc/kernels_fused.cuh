@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "kernels_act.cuh"
 #include "kernels_stream.cuh"
 
 namespace iabn {
@@ -290,7 +291,10 @@ __device__ __forceinline__ float lds_elem(uint32_t addr) {
 // ~100 KB slabs: large channels) or 4 (up to 56 registers, ~50 KB slabs: small
 // layers, where more resident pipelines hide the per-channel latency)
 // MIS: planes not 16-byte aligned (e.g. bf16 14x14): covering ranges, masked edges
-template <typename T, int PASS, int MINB, bool MIS = false>
+// ACT: 0 leaky ReLU (slope a), 1 sigmoid, 2 tanh (kernels_act.cuh; fp32 only):
+// the reduce takes dy = f'(z) dz and y = f^-1(z) per element, the apply z = f(y) /
+// dx = alpha dy + kappa y + cc; everything else (slabs, records, coefficients) is shared.
+template <typename T, int PASS, int MINB, bool MIS = false, int ACT = 0>
 __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedArgs a) {
     constexpr int NIN = PASS == 0 ? 1 : 2;
     constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
@@ -795,6 +799,18 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         s1[i] = add2(s1[i], d[i]);
                         s2[i] = fma2(d[i], d[i], s2[i]);
                     }
+                } else if constexpr (ACT != 0) {  // dy = f'(z) dz, y = f^-1(z)
+                    float2 zz[NP], dd[NP];
+                    Pairs<T>::load(zu, zz);
+                    Pairs<T>::load(du, dd);
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) {
+                        const float2 dy = make_float2(Act<ACT>::df(zz[i].x) * dd[i].x,
+                                                      Act<ACT>::df(zz[i].y) * dd[i].y);
+                        const float2 y = make_float2(Act<ACT>::inv(zz[i].x), Act<ACT>::inv(zz[i].y));
+                        s1[i] = add2(s1[i], dy);
+                        s2[i] = V2 ? fma2(dy, y, s2[i]) : fma2(dy, fma2(y, ig2, nb2), s2[i]);
+                    }
                 } else if (V2 && sizeof(T) == 2) {
                     const uint32_t zw[4] = {zu.x, zu.y, zu.z, zu.w};
                     const uint32_t dw[4] = {du.x, du.y, du.z, du.w};
@@ -840,6 +856,12 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         const float d = ok ? zz[k] - K0 : 0.f;
                         *a1 += d;
                         *a2 = fmaf(d, d, *a2);
+                    } else if constexpr (ACT != 0) {
+                        // selects, not products: a masked element may be anything
+                        const float dy = Act<ACT>::df(zz[k]) * dd[k];
+                        const float t2 = dy * (V2 ? Act<ACT>::inv(zz[k]) : fmaf(Act<ACT>::inv(zz[k]), ig2.x, nb2.x));
+                        *a1 += ok ? dy : 0.f;
+                        *a2 += ok ? t2 : 0.f;
                     } else if (V2 && sizeof(T) == 2) {
                         float* an = (k & 1) ? &sn[k >> 1].y : &sn[k >> 1].x;
                         *a1 += ok ? dd[k] : 0.f;
@@ -1036,8 +1058,23 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
                     const float2 y = fma2(w[i], P, Q2);
-                    const float2 ay = mul2(y, sl2);  // f(y) = max(y, a y) for 0 < a <= 1
-                    w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                    if constexpr (ACT != 0) {
+                        w[i] = make_float2(Act<ACT>::f(y.x), Act<ACT>::f(y.y));
+                    } else {
+                        const float2 ay = mul2(y, sl2);  // f(y) = max(y, a y) for 0 < a <= 1
+                        w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                    }
+                }
+            } else if constexpr (ACT != 0) {  // dx = alpha f'(z) dz + kappa f^-1(z) + cc
+                float2 dd[NP];
+                Pairs<T>::load(xu, w);
+                Pairs<T>::load(du, dd);
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                    const float2 dy = make_float2(Act<ACT>::df(w[i].x) * dd[i].x,
+                                                  Act<ACT>::df(w[i].y) * dd[i].y);
+                    const float2 y = make_float2(Act<ACT>::inv(w[i].x), Act<ACT>::inv(w[i].y));
+                    w[i] = fma2(make_float2(P.x, P.x), dy, fma2(make_float2(P.y, P.y), y, make_float2(mu, mu)));
                 }
             } else {
                 float2 dd[NP];
@@ -1079,8 +1116,23 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
 #pragma unroll
                     for (int j = 0; j < NP; ++j) {
                         const float2 y = fma2(w[j], P, Q2);
-                        const float2 ay = mul2(y, sl2);
-                        w[j] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                        if constexpr (ACT != 0) {
+                            w[j] = make_float2(Act<ACT>::f(y.x), Act<ACT>::f(y.y));
+                        } else {
+                            const float2 ay = mul2(y, sl2);
+                            w[j] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
+                        }
+                    }
+                } else if constexpr (ACT != 0) {
+                    float2 dd[NP];
+                    Pairs<T>::load(xu, w);
+                    Pairs<T>::load(du, dd);
+#pragma unroll
+                    for (int j = 0; j < NP; ++j) {
+                        const float2 dy = make_float2(Act<ACT>::df(w[j].x) * dd[j].x,
+                                                      Act<ACT>::df(w[j].y) * dd[j].y);
+                        const float2 y = make_float2(Act<ACT>::inv(w[j].x), Act<ACT>::inv(w[j].y));
+                        w[j] = fma2(make_float2(P.x, P.x), dy, fma2(make_float2(P.y, P.y), y, make_float2(mu, mu)));
                     }
                 } else {
                     float2 dd[NP];

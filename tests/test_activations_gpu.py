@@ -1,6 +1,7 @@
 """BN followed by sigmoid / tanh ("Many activation functions are actually
 invertible ... sigmoid, hyperbolic tangent, Leaky ReLU"): the CUDA path
-(IABN_ACT_SIGMOID / IABN_ACT_TANH, kernels_act.cuh) against the oracle's
+(IABN_ACT_SIGMOID / IABN_ACT_TANH: the channel-resident kernels for NCHW, the streaming
+kernels of kernels_act.cuh otherwise) against the oracle's
 forward_act / backward_inplace_act / backward_standard_act (fp64), element by element,
 through the C ABI.  The activations are smooth, so no branch allowance (R16) applies:
 per-channel normwise error <= 1e-4 (fp32 storage, BASELINE.json north_star)."""
@@ -85,19 +86,40 @@ def test_act_parity(case, act):
     assert all(v <= TOL for v in errs.values()), errs
 
 
+@pytest.mark.parametrize("flags", [0, 1 << 8], ids=["auto", "streaming"])
 @pytest.mark.parametrize("act", ACTS)
-def test_act_out_of_place_and_variant_flag(act):
-    """Out-of-place equals in-place bit for bit; IABN_VARIANT_I changes nothing (both
-    variants need f^-1(z) per element, kernels_act.cuh)."""
+def test_act_out_of_place_and_variants(act, flags):
+    """Out-of-place equals in-place bit for bit, on the channel-resident and the streaming
+    schedule; IABN_VARIANT_I (per-element dy x^) and the default II (sum dy y, then
+    (Q - beta S1)/g) agree with each other and with the oracle."""
     from paper_1712_02616_b200 import _lib as L
     case = Case(4, 20, 100, seed=98)
     x, dz, p = inputs(case)
-    a = _run_gpu(case, x, dz, p, act)
-    b = _run_gpu(case, x, dz, p, act, inplace=False)
-    c = _run_gpu(case, x, dz, p, act, flags=L.VARIANT_I)
+    a = _run_gpu(case, x, dz, p, act, flags=flags)
+    b = _run_gpu(case, x, dz, p, act, flags=flags, inplace=False)
+    c = _run_gpu(case, x, dz, p, act, flags=flags | L.VARIANT_I)
+    ref = _ref(case, x, dz, p, act)
     for k in a:
         assert torch.equal(a[k], b[k]), k
-        assert torch.equal(a[k], c[k]), k
+    for got in (a, c):
+        errs = _errs(case, got, ref)
+        assert all(v <= TOL for v in errs.values()), errs
+
+
+@pytest.mark.parametrize("act", ACTS)
+def test_act_schedules_agree(act):
+    """The channel-resident schedule (NCHW default, covering-range variant for the
+    misaligned fp32 plane of 7x11) and the streaming one, both against the oracle."""
+    from paper_1712_02616_b200 import _lib as L
+    for case in (Case(8, 48, 196, seed=101), Case(6, 24, 77, seed=102)):
+        d = L.desc(case.N, case.C, case.HW, L.F32, L.NCHW)
+        flag = L.ACT_SIGMOID if act == "sigmoid" else L.ACT_TANH
+        assert L.query_schedule(d, 0, flag)[0] == 1 and L.query_schedule(d, 1, flag)[0] == 1
+        x, dz, p = inputs(case)
+        ref = _ref(case, x, dz, p, act)
+        for fl in (0, 1 << 8):
+            errs = _errs(case, _run_gpu(case, x, dz, p, act, flags=fl), ref)
+            assert all(v <= TOL for v in errs.values()), (fl, errs)
 
 
 @pytest.mark.parametrize("layout", ["NCHW", "NHWC"])
@@ -184,6 +206,7 @@ def test_act_rejections_and_schedule():
     st = P.forward_reduce(x)
     with pytest.raises(L.IabnError):
         P.forward_apply(x.clone(), st, g, b, flags=L.ACT_SIGMOID)
-    d = L.desc(32, 64, 3136, L.F32, L.NCHW)
+    d = L.desc(32, 64, 3136, L.F32, L.NHWC)  # NHWC: streaming
     for pass_ in (0, 1):
         assert tuple(L.query_schedule(d, pass_, L.ACT_TANH)) == (0, 0)
+        assert tuple(L.query_schedule(d, pass_, L.ACT_TANH | (1 << 8))) == (0, 0)
