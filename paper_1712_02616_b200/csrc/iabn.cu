@@ -947,7 +947,7 @@ SmallPlan small_plan(const Geom& g, uint32_t flags, int sms) {
     return p;
 }
 
-template <typename T>
+template <typename T, int ACT = 0>
 iabn_status launch_small(int pass, const Geom& g, const SmallPlan& p, SmallArgs a, cudaStream_t st) {
     a.C = g.C;
     a.HW = g.HW;
@@ -971,11 +971,11 @@ iabn_status launch_small(int pass, const Geom& g, const SmallPlan& p, SmallArgs 
         g_trace_ch = (uint32_t)kSmallTrace;
     }
     if (p.R == 4) {
-        if (pass == 0) launch_pdl(small_kernel<T, 0, 4>, p.grid, kSmallThreads, 0, st, a);
-        else launch_pdl(small_kernel<T, 1, 4>, p.grid, kSmallThreads, 0, st, a);
+        if (pass == 0) launch_pdl(small_kernel<T, 0, 4, ACT>, p.grid, kSmallThreads, 0, st, a);
+        else launch_pdl(small_kernel<T, 1, 4, ACT>, p.grid, kSmallThreads, 0, st, a);
     } else {
-        if (pass == 0) launch_pdl(small_kernel<T, 0, 8>, p.grid, kSmallThreads, 0, st, a);
-        else launch_pdl(small_kernel<T, 1, 8>, p.grid, kSmallThreads, 0, st, a);
+        if (pass == 0) launch_pdl(small_kernel<T, 0, 8, ACT>, p.grid, kSmallThreads, 0, st, a);
+        else launch_pdl(small_kernel<T, 1, 8, ACT>, p.grid, kSmallThreads, 0, st, a);
     }
     return check_launch(pass == 0 ? "small_kernel<fwd>" : "small_kernel<bwd>");
 }
@@ -1870,6 +1870,27 @@ iabn_status act_reduce(const Geom& g, int S, const float* z, const float* dz, co
 iabn_status act_forward(const Ctx& c, const float* x, float* z, const float* gamma,
                         const float* beta, float* rm, float* rv, float* sm, float* sv,
                         float momentum, float eps, uint32_t flags) {
+    if (!(flags & (IABN_EVAL | IABN_FORCE_STREAMING | IABN_FORCE_FUSED))) {  // small NCHW layers
+        const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
+        if (sp.ok) {
+            SmallArgs a{};
+            a.in0 = x;
+            a.out = z;
+            a.gamma = gamma;
+            a.beta = beta;
+            a.running_mean = rm;
+            a.running_var = rv;
+            a.save_mean = sm;
+            a.save_var = sv;
+            a.momentum = momentum;
+            a.eps = eps;
+            a.slope = 1.f;
+            a.inv_slope = 1.f;
+            a.flags = flags;
+            return (flags & IABN_ACT_SIGMOID) ? launch_small<float, 1>(0, c.g, sp, a, c.st)
+                                              : launch_small<float, 2>(0, c.g, sp, a, c.st);
+        }
+    }
     if (!(flags & (IABN_EVAL | IABN_FORCE_STREAMING))) {  // NCHW: the channel-resident kernels
         const FusedPlan p = fused_plan(c.g, 0, *c.dev, flags);
         if (p.ok) {
@@ -1899,6 +1920,25 @@ iabn_status act_backward(const Ctx& c, const float* z, const float* dz, float* d
                          const float* gamma, const float* beta, const float* sv, float* dg,
                          float* db, float eps, uint32_t flags) {
     const bool sig = flags & IABN_ACT_SIGMOID;
+    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED))) {  // small NCHW layers
+        const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
+        if (sp.ok) {
+            SmallArgs a{};
+            a.in0 = z;
+            a.in1 = dz;
+            a.out = dx;
+            a.gamma = gamma;
+            a.beta = beta;
+            a.save_var = const_cast<float*>(sv);
+            a.dgamma = dg;
+            a.dbeta = db;
+            a.eps = eps;
+            a.slope = 1.f;
+            a.inv_slope = 1.f;
+            a.flags = flags;
+            return sig ? launch_small<float, 1>(1, c.g, sp, a, c.st) : launch_small<float, 2>(1, c.g, sp, a, c.st);
+        }
+    }
     if (!(flags & IABN_FORCE_STREAMING)) {
         const FusedPlan p = fused_plan(c.g, 1, *c.dev, flags);
         if (p.ok) {
@@ -2207,8 +2247,14 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
     if (pass != 0 && pass != 1) return fail(IABN_ERR_INVALID_ARG, "pass must be 0 or 1");
     DevFacts* dev;
     IABN_TRY(device_facts(&dev));
-    if (act_of(flags)) {  // sigmoid / tanh: channel-resident (NCHW) or streaming
+    if (act_of(flags)) {  // sigmoid / tanh: small / channel-resident (NCHW) or streaming
         IABN_TRY(check_act_flags(g, flags));
+        if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_FUSED)) &&
+            small_plan(g, flags, dev->sms).ok) {
+            *schedule = 5;
+            *cluster = 0;
+            return IABN_OK;
+        }
         FusedPlan p;
         if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL))) p = fused_plan(g, pass, *dev, flags);
         *schedule = p.ok ? 1 : 0;

@@ -22,6 +22,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernels_act.cuh"
 #include "kernels_stream.cuh"
 
 namespace iabn {
@@ -72,7 +73,8 @@ __device__ __forceinline__ uint4 ldg_coherent(const void* p) {
     return r;
 }
 
-template <typename T, int PASS, int R>
+// ACT: 0 leaky ReLU, 1 sigmoid, 2 tanh (fp32 only; kernels_act.cuh)
+template <typename T, int PASS, int R, int ACT = 0>
 __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMALL_MINB_F4 : 4) : (PASS == 0 ? 3 : 2))
     small_kernel(const SmallArgs a) {
     constexpr int V = Elem<T>::kVec;
@@ -160,6 +162,13 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
                 const float d = ok ? x - K0 : 0.f;
                 s1 += d;
                 s2 = fmaf(d, d, s2);
+            } else if constexpr (ACT != 0) {  // dy = f'(z) dz, y = f^-1(z); selects (masked
+                                              // slots may hold anything)
+                const float dy = Act<ACT>::df(x) * ((e & 1) ? q[e >> 1].y : q[e >> 1].x);
+                const float y = Act<ACT>::inv(x);
+                const float t3 = (a.flags & kVariantI) ? dy * ((y - bet) * ig) : dy * y;
+                s1 += ok ? dy : 0.f;
+                s3 += ok ? t3 : 0.f;
             } else {
                 const float dz = ok ? ((e & 1) ? q[e >> 1].y : q[e >> 1].x) : 0.f;
                 s1 += dz;
@@ -257,7 +266,14 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
         for (int e = 0; e < NP; ++e) {
             if (PASS == 0) {
                 const float y0 = fmaf(p[e].x - c1, c0, c2), y1 = fmaf(p[e].y - c1, c0, c2);
-                w[e] = make_float2(y0 >= 0.f ? y0 : y0 * a.slope, y1 >= 0.f ? y1 : y1 * a.slope);
+                if constexpr (ACT != 0)
+                    w[e] = make_float2(Act<ACT>::f(y0), Act<ACT>::f(y1));
+                else
+                    w[e] = make_float2(y0 >= 0.f ? y0 : y0 * a.slope, y1 >= 0.f ? y1 : y1 * a.slope);
+            } else if constexpr (ACT != 0) {  // dx = alpha dy + kappa y + cc
+                const float z0 = p[e].x, z1 = p[e].y;
+                w[e].x = fmaf(c0, Act<ACT>::df(z0) * q[e].x, fmaf(c1, Act<ACT>::inv(z0), c4));
+                w[e].y = fmaf(c0, Act<ACT>::df(z1) * q[e].y, fmaf(c1, Act<ACT>::inv(z1), c4));
             } else {
                 const float z0 = p[e].x, z1 = p[e].y;
                 w[e].x = z0 >= 0.f ? fmaf(c0, q[e].x, fmaf(c1, z0, c4)) : fmaf(c2, q[e].x, fmaf(c3, z0, c4));

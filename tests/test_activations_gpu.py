@@ -108,16 +108,22 @@ def test_act_out_of_place_and_variants(act, flags):
 
 @pytest.mark.parametrize("act", ACTS)
 def test_act_schedules_agree(act):
-    """The channel-resident schedule (NCHW default, covering-range variant for the
-    misaligned fp32 plane of 7x11) and the streaming one, both against the oracle."""
+    """Every NCHW schedule with the activation as a template parameter -- register-resident
+    small layers (default here), channel-resident (IABN_FORCE_FUSED; covering-range variant
+    for the misaligned fp32 plane of 7x11), streaming -- against the oracle, both
+    variants."""
     from paper_1712_02616_b200 import _lib as L
-    for case in (Case(8, 48, 196, seed=101), Case(6, 24, 77, seed=102)):
+    flag = L.ACT_SIGMOID if act == "sigmoid" else L.ACT_TANH
+    for case in (Case(8, 48, 196, seed=101), Case(6, 24, 77, seed=102),
+                 Case(32, 40, 49, seed=103)):
         d = L.desc(case.N, case.C, case.HW, L.F32, L.NCHW)
-        flag = L.ACT_SIGMOID if act == "sigmoid" else L.ACT_TANH
-        assert L.query_schedule(d, 0, flag)[0] == 1 and L.query_schedule(d, 1, flag)[0] == 1
+        for pass_ in (0, 1):
+            assert L.query_schedule(d, pass_, flag)[0] == 5
+            assert L.query_schedule(d, pass_, flag | L.FORCE_FUSED)[0] == 1
+            assert L.query_schedule(d, pass_, flag | L.FORCE_STREAMING)[0] == 0
         x, dz, p = inputs(case)
         ref = _ref(case, x, dz, p, act)
-        for fl in (0, 1 << 8):
+        for fl in (0, L.FORCE_FUSED, L.FORCE_STREAMING, L.VARIANT_I, L.FORCE_FUSED | L.VARIANT_I):
             errs = _errs(case, _run_gpu(case, x, dz, p, act, flags=fl), ref)
             assert all(v <= TOL for v in errs.values()), (fl, errs)
 
