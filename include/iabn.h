@@ -117,8 +117,8 @@ enum {
        only (the split-phase and synchronized entries return IABN_ERR_UNSUPPORTED), fp32
        storage only (IABN_ERR_UNSUPPORTED for bf16: the inverse of an 8-bit-mantissa
        sigmoid / tanh output is ill-conditioned); the small-layer and channel-resident
-       schedules for NCHW (IABN_FORCE_FUSED / IABN_FORCE_STREAMING select), streaming
-       otherwise.  The backward
+       schedules for NCHW, the channel-group schedule for NHWC (IABN_FORCE_FUSED /
+       IABN_FORCE_STREAMING select), streaming otherwise.  The backward
        inverts z: x^ = (f^-1(z) - beta)/g, dy = f'(z) dz (Alg. 2), with z clamped into
        the open range of f first (saturated outputs, R17); variant II sums
        dy y and forms (Q - beta S1)/g per channel, IABN_VARIANT_I sums dy x^. */

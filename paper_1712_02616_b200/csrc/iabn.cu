@@ -126,12 +126,19 @@ iabn_status device_facts(DevFacts** out) {
                               (const void*)nhwc_fused_kernel<float, 1>,
                               (const void*)nhwc_fused_kernel<__nv_bfloat16, 1>};
         for (const void* fn : nhwc) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        const void* nhwc_act[] = {(const void*)nhwc_fused_kernel<float, 0, 1>, (const void*)nhwc_fused_kernel<float, 1, 1>,
+                                  (const void*)nhwc_fused_kernel<float, 0, 2>, (const void*)nhwc_fused_kernel<float, 1, 2>};
+        for (const void* fn : nhwc_act) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         const void* nb[] = {(const void*)nhwc_bulk_reduce_kernel<float, 0, false>,
                             (const void*)nhwc_bulk_reduce_kernel<float, 1, false>,
                             (const void*)nhwc_bulk_reduce_kernel<float, 1, true>,
                             (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 0, false>,
                             (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 1, false>,
-                            (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 1, true>};
+                            (const void*)nhwc_bulk_reduce_kernel<__nv_bfloat16, 1, true>,
+                            (const void*)nhwc_bulk_reduce_kernel<float, 1, false, 1>,
+                            (const void*)nhwc_bulk_reduce_kernel<float, 1, true, 1>,
+                            (const void*)nhwc_bulk_reduce_kernel<float, 1, false, 2>,
+                            (const void*)nhwc_bulk_reduce_kernel<float, 1, true, 2>};
         for (const void* fn : nb) {
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNbSmem);
             cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1016,7 +1023,7 @@ iabn_status nhwc_tmap(CUtensorMap* tm, const void* ptr, const Geom& g, const Nhw
     return IABN_OK;
 }
 
-template <typename T>
+template <typename T, int ACT = 0>
 iabn_status launch_nhwc(int pass, const Geom& g, const NhwcPlan& p, NhwcArgs a, const void* in0,
                         const void* in1, void* out, cudaStream_t st) {
     CUtensorMap t0, t1, t2;
@@ -1072,8 +1079,8 @@ iabn_status launch_nhwc(int pass, const Geom& g, const NhwcPlan& p, NhwcArgs a, 
     }
     cfg.attrs = at;
     cfg.numAttrs = na;
-    const cudaError_t e = pass == 0 ? cudaLaunchKernelEx(&cfg, nhwc_fused_kernel<T, 0>, t0, t1, t2, a)
-                                    : cudaLaunchKernelEx(&cfg, nhwc_fused_kernel<T, 1>, t0, t1, t2, a);
+    const cudaError_t e = pass == 0 ? cudaLaunchKernelEx(&cfg, nhwc_fused_kernel<T, 0, ACT>, t0, t1, t2, a)
+                                    : cudaLaunchKernelEx(&cfg, nhwc_fused_kernel<T, 1, ACT>, t0, t1, t2, a);
     if (e != cudaSuccess) {
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return fail(IABN_ERR_CUDA, "nhwc launch: %s", cudaGetErrorString(e));
@@ -1157,7 +1164,7 @@ iabn_status launch_gres(const Geom& g, int G, GresArgs a, cudaStream_t st) {
 }
 
 // ====================================================================== streaming launches
-template <typename T, int PASS>
+template <typename T, int PASS, int ACT = 0>
 iabn_status launch_nb(const Geom& g, int S, const void* in0, const void* in1, const float* gamma,
                       const float* beta, float eps, float slope, uint32_t flags, double* part,
                       cudaStream_t st) {
@@ -1216,9 +1223,9 @@ iabn_status launch_nb(const Geom& g, int S, const void* in0, const void* in1, co
     if (PASS == 0)
         cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 0, false>, a);
     else if (flags & IABN_VARIANT_I)
-        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 1, false>, a);
+        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 1, false, ACT>, a);
     else
-        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 1, true>, a);
+        cudaLaunchKernelEx(&cfg, nhwc_bulk_reduce_kernel<T, 1, true, ACT>, a);
     return check_launch(PASS == 0 ? "nhwc_bulk_reduce<stats>" : "nhwc_bulk_reduce<grad>");
 }
 
@@ -1899,6 +1906,23 @@ iabn_status act_forward(const Ctx& c, const float* x, float* z, const float* gam
             return (flags & IABN_ACT_SIGMOID) ? launch_fused<float, 1>(0, p, a, c.st)
                                               : launch_fused<float, 2>(0, p, a, c.st);
         }
+        const NhwcPlan np = nhwc_plan(c.g, 0, *c.dev, flags);  // NHWC: channel groups
+        if (np.ok) {
+            NhwcArgs a{};
+            a.gamma = gamma;
+            a.beta = beta;
+            a.running_mean = rm;
+            a.running_var = rv;
+            a.save_mean = sm;
+            a.save_var = sv;
+            a.momentum = momentum;
+            a.eps = eps;
+            a.slope = 1.f;
+            a.inv_slope = 1.f;
+            a.flags = flags;
+            return (flags & IABN_ACT_SIGMOID) ? launch_nhwc<float, 1>(0, c.g, np, a, x, nullptr, z, c.st)
+                                              : launch_nhwc<float, 2>(0, c.g, np, a, x, nullptr, z, c.st);
+        }
     }
     float4* coef = wsp<float4>(c, c.w.coef);
     if (flags & IABN_EVAL) {
@@ -1946,13 +1970,36 @@ iabn_status act_backward(const Ctx& c, const float* z, const float* dz, float* d
                                                flags);
             return sig ? launch_fused<float, 1>(1, p, a, c.st) : launch_fused<float, 2>(1, p, a, c.st);
         }
+        const NhwcPlan np = nhwc_plan(c.g, 1, *c.dev, flags);  // NHWC: channel groups
+        if (np.ok) {
+            NhwcArgs a{};
+            a.gamma = gamma;
+            a.beta = beta;
+            a.save_var = const_cast<float*>(sv);
+            a.dgamma = dg;
+            a.dbeta = db;
+            a.eps = eps;
+            a.slope = 1.f;
+            a.inv_slope = 1.f;
+            a.flags = flags;
+            return sig ? launch_nhwc<float, 1>(1, c.g, np, a, z, dz, dx, c.st)
+                       : launch_nhwc<float, 2>(1, c.g, np, a, z, dz, dx, c.st);
+        }
     }
     double* part = wsp<double>(c, c.w.part);
     float4* coef = wsp<float4>(c, c.w.coef);
-    // NHWC: the LDG splits (c.S may count bulk-ring clusters), within the workspace's 296
-    const int S = c.g.layout == IABN_NHWC ? (int)std::min<int64_t>(stat_splits_ldg(c.g), kGresMaxG) : c.S;
-    IABN_TRY(sig ? act_reduce<1>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st)
-                 : act_reduce<2>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st));
+    // NHWC: the bulk-ring reduction when it applies (c.S = its cluster records), else the
+    // LDG splits within the workspace's 296 records
+    int S = c.S;
+    if (c.g.layout == IABN_NHWC && nb_grid(c.g)) {
+        const iabn_status st = sig ? launch_nb<float, 1, 1>(c.g, S, z, dz, gamma, beta, eps, 1.f, flags, part, c.st)
+                                   : launch_nb<float, 1, 2>(c.g, S, z, dz, gamma, beta, eps, 1.f, flags, part, c.st);
+        IABN_TRY(st);
+    } else {
+        if (c.g.layout == IABN_NHWC) S = (int)std::min<int64_t>(stat_splits_ldg(c.g), kGresMaxG);
+        IABN_TRY(sig ? act_reduce<1>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st)
+                     : act_reduce<2>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st));
+    }
     BwdCoefArgs a{part, S, part, S, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg, db,
                   coef, eps, flags};
     launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
@@ -2259,6 +2306,13 @@ iabn_status iabn_query_schedule(const iabn_desc* desc, int pass, uint32_t flags,
         if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL))) p = fused_plan(g, pass, *dev, flags);
         *schedule = p.ok ? 1 : 0;
         *cluster = p.ok ? p.K : 0;
+        if (!p.ok && !(flags & (IABN_FORCE_STREAMING | IABN_EVAL))) {
+            const NhwcPlan np = nhwc_plan(g, pass, *dev, flags);
+            if (np.ok) {
+                *schedule = 4;
+                *cluster = (int)np.K;
+            }
+        }
         return IABN_OK;
     }
     if (!(flags & (IABN_FORCE_STREAMING | IABN_EVAL | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {

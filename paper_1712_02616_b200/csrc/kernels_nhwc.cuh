@@ -32,6 +32,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "kernels_act.cuh"
 #include "kernels_stream.cuh"
 
 namespace iabn {
@@ -123,7 +124,8 @@ __device__ __forceinline__ void mbar_wait_nhwc(uint64_t* bar, uint32_t parity) {
 
 // ------------------------------------------------------------------ kernel
 // PASS 0 forward (in0 = x, out = z), PASS 1 backward (in0 = z, in1 = dz, out = dx).
-template <typename T, int PASS>
+// ACT: 0 leaky ReLU, 1 sigmoid, 2 tanh (fp32 only; kernels_act.cuh)
+template <typename T, int PASS, int ACT = 0>
 __global__ void __launch_bounds__(kNhwcThreads, 1)
     nhwc_fused_kernel(const __grid_constant__ CUtensorMap tm_in0,
                       const __grid_constant__ CUtensorMap tm_in1,
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kNhwcThreads, 1)
             }
         }
         float betav[V], ginv[V];
-        if (PASS == 1 && (a.flags & kVariantI)) {
+        if (PASS == 1 && (ACT != 0 || (a.flags & kVariantI))) {
 #pragma unroll
             for (int k = 0; k < V; ++k) {
                 const int64_t c = (int64_t)c0 + cbase + k;
@@ -262,22 +264,36 @@ __global__ void __launch_bounds__(kNhwcThreads, 1)
             float2 zz[NP], dd[NP];
             Pairs<T>::load(uz, zz);
             Pairs<T>::load(ud, dd);
+            if constexpr (ACT != 0) {  // s1 = sum dy, s3 = sum dy y (II) / dy x^ (I), s2 = 0
 #pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const float2 neg = make_float2(zz[p].x < 0.f ? dd[p].x : 0.f,
-                                               zz[p].y < 0.f ? dd[p].y : 0.f);
-                s1[p] = add2(s1[p], dd[p]);   // sum dz
-                s2[p] = add2(s2[p], neg);     // sum_{z<0} dz
-                if (a.flags & kVariantI) {
-                    // dy x^ with dy, y on the branch of sign(z)
-                    const float y0 = zz[p].x >= 0.f ? zz[p].x : zz[p].x * inv_slope;
-                    const float y1 = zz[p].y >= 0.f ? zz[p].y : zz[p].y * inv_slope;
-                    const float dy0 = zz[p].x >= 0.f ? dd[p].x : dd[p].x * slope;
-                    const float dy1 = zz[p].y >= 0.f ? dd[p].y : dd[p].y * slope;
-                    s3[p].x = fmaf(dy0, (y0 - betav[2 * p]) * ginv[2 * p], s3[p].x);
-                    s3[p].y = fmaf(dy1, (y1 - betav[2 * p + 1]) * ginv[2 * p + 1], s3[p].y);
-                } else {
-                    s3[p] = fma2(dd[p], zz[p], s3[p]);  // sum dz z = sum dy y
+                for (int p = 0; p < NP; ++p) {
+                    const float2 dy = make_float2(Act<ACT>::df(zz[p].x) * dd[p].x,
+                                                  Act<ACT>::df(zz[p].y) * dd[p].y);
+                    float2 y = make_float2(Act<ACT>::inv(zz[p].x), Act<ACT>::inv(zz[p].y));
+                    if (a.flags & kVariantI)
+                        y = make_float2((y.x - betav[2 * p]) * ginv[2 * p],
+                                        (y.y - betav[2 * p + 1]) * ginv[2 * p + 1]);
+                    s1[p] = add2(s1[p], dy);
+                    s3[p] = fma2(dy, y, s3[p]);
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < NP; ++p) {
+                    const float2 neg = make_float2(zz[p].x < 0.f ? dd[p].x : 0.f,
+                                                   zz[p].y < 0.f ? dd[p].y : 0.f);
+                    s1[p] = add2(s1[p], dd[p]);   // sum dz
+                    s2[p] = add2(s2[p], neg);     // sum_{z<0} dz
+                    if (a.flags & kVariantI) {
+                        // dy x^ with dy, y on the branch of sign(z)
+                        const float y0 = zz[p].x >= 0.f ? zz[p].x : zz[p].x * inv_slope;
+                        const float y1 = zz[p].y >= 0.f ? zz[p].y : zz[p].y * inv_slope;
+                        const float dy0 = zz[p].x >= 0.f ? dd[p].x : dd[p].x * slope;
+                        const float dy1 = zz[p].y >= 0.f ? dd[p].y : dd[p].y * slope;
+                        s3[p].x = fmaf(dy0, (y0 - betav[2 * p]) * ginv[2 * p], s3[p].x);
+                        s3[p].y = fmaf(dy1, (y1 - betav[2 * p + 1]) * ginv[2 * p + 1], s3[p].y);
+                    } else {
+                        s3[p] = fma2(dd[p], zz[p], s3[p]);  // sum dz z = sum dy y
+                    }
                 }
             }
         };
@@ -457,8 +473,13 @@ __global__ void __launch_bounds__(kNhwcThreads, 1)
                 for (int p = 0; p < NP; ++p) {
                     float y0 = fmaf(f[p].x - M[2 * p], A[2 * p], B[2 * p]);
                     float y1 = fmaf(f[p].y - M[2 * p + 1], A[2 * p + 1], B[2 * p + 1]);
-                    f[p].x = y0 >= 0.f ? y0 : y0 * slope;
-                    f[p].y = y1 >= 0.f ? y1 : y1 * slope;
+                    if constexpr (ACT != 0) {
+                        f[p].x = Act<ACT>::f(y0);
+                        f[p].y = Act<ACT>::f(y1);
+                    } else {
+                        f[p].x = y0 >= 0.f ? y0 : y0 * slope;
+                        f[p].y = y1 >= 0.f ? y1 : y1 * slope;
+                    }
                 }
                 const uint4 o = Pairs<T>::store(f);
                 asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(o.x),
@@ -494,6 +515,13 @@ __global__ void __launch_bounds__(kNhwcThreads, 1)
 #pragma unroll
                 for (int p = 0; p < NP; ++p) {
                     const int k0 = 2 * p, k1 = 2 * p + 1;
+                    if constexpr (ACT != 0) {  // dx = alpha dy + kappa y + cc
+                        dd[p].x = fmaf(al[k0], Act<ACT>::df(zz[p].x) * dd[p].x,
+                                       fmaf(ka[k0], Act<ACT>::inv(zz[p].x), cc[k0]));
+                        dd[p].y = fmaf(al[k1], Act<ACT>::df(zz[p].y) * dd[p].y,
+                                       fmaf(ka[k1], Act<ACT>::inv(zz[p].y), cc[k1]));
+                        continue;
+                    }
                     dd[p].x = zz[p].x >= 0.f ? fmaf(al[k0], dd[p].x, fmaf(ka[k0], zz[p].x, cc[k0]))
                                              : fmaf(aln[k0], dd[p].x, fmaf(kan[k0], zz[p].x, cc[k0]));
                     dd[p].y = zz[p].y >= 0.f ? fmaf(al[k1], dd[p].y, fmaf(ka[k1], zz[p].y, cc[k1]))

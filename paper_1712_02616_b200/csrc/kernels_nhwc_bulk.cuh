@@ -20,6 +20,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernels_act.cuh"
 #include "kernels_stream.cuh"
 
 namespace iabn {
@@ -53,7 +54,9 @@ constexpr int kNbCluster = 8;  // CTAs per cluster: their records are summed ove
 // PASS 0: F1 shifted sums (sum d, sum d^2), d = x - K.  PASS 1, V2 (default, InPlace-ABN II
 // as in the channel-resident kernels, R6): (sum dz, sum_{z<0} dz, sum dz z);
 // PASS 1, !V2 (IABN_VARIANT_I): (sum dy, sum dy x^) per element.
-template <typename T, int PASS, bool V2>
+// ACT (fp32, PASS 1): 1 sigmoid / 2 tanh -- (sum dy, 0, sum dy y) with dy = f'(z) dz,
+// y = f^-1(z) (V2), or (sum dy, sum dy x^) (!V2)
+template <typename T, int PASS, bool V2, int ACT = 0>
 __global__ void __launch_bounds__(kThreads, 2) nhwc_bulk_reduce_kernel(const NbArgs a) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 2) nhwc_bulk_reduce_kernel(const NbA
     // per-channel constants of this thread's vector j (channels j*V .. j*V + V-1)
     const int64_t c0 = (int64_t)j * V;
     float2 nK[NP];              // F1: -K (shift = the channel's first value)
-    InvAffine ia[PASS == 1 && !V2 ? V : 1];
+    InvAffine ia[PASS == 1 && !V2 ? V : 1];  // (inv_g, -beta/g) per channel
 #pragma unroll
     for (int i = 0; i < NP; ++i) nK[i] = make_float2(0.f, 0.f);
     if (PASS == 0) {
@@ -171,7 +174,22 @@ __global__ void __launch_bounds__(kThreads, 2) nhwc_bulk_reduce_kernel(const NbA
                 }
             } else {
                 const uint4 w = lds128(base + SB + r * rowb);
-                if constexpr (V2) {
+                if constexpr (ACT != 0) {
+                    float2 zp[NP], dp[NP];
+                    Pairs<T>::load(u, zp);
+                    Pairs<T>::load(w, dp);
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) {
+                        const float2 dy = make_float2(Act<ACT>::df(zp[i].x) * dp[i].x,
+                                                      Act<ACT>::df(zp[i].y) * dp[i].y);
+                        float2 y = make_float2(Act<ACT>::inv(zp[i].x), Act<ACT>::inv(zp[i].y));
+                        if constexpr (!V2)  // x^ = y inv_g + nb
+                            y = make_float2(fmaf(y.x, ia[2 * i].inv_g, ia[2 * i].nb),
+                                            fmaf(y.y, ia[2 * i + 1].inv_g, ia[2 * i + 1].nb));
+                        acc[0][i] = add2(acc[0][i], dy);
+                        acc[NA - 1][i] = fma2(dy, y, acc[NA - 1][i]);
+                    }
+                } else if constexpr (V2) {
                     if constexpr (sizeof(T) == 2) {  // packed bf16 ops (no unpacking)
                         const uint32_t zw[4] = {u.x, u.y, u.z, u.w}, dw[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll

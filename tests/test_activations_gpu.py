@@ -216,3 +216,21 @@ def test_act_rejections_and_schedule():
     for pass_ in (0, 1):
         assert tuple(L.query_schedule(d, pass_, L.ACT_TANH)) == (0, 0)
         assert tuple(L.query_schedule(d, pass_, L.ACT_TANH | (1 << 8))) == (0, 0)
+
+
+@pytest.mark.parametrize("act", ACTS)
+def test_act_nhwc_channel_groups(act):
+    """NHWC layers whose channel groups fit on chip take the channel-group kernels with the
+    activation as a template parameter (schedule 4); against the oracle with both
+    variants, and against the streaming schedule's result."""
+    from paper_1712_02616_b200 import _lib as L
+    flag = L.ACT_SIGMOID if act == "sigmoid" else L.ACT_TANH
+    for case in (Case(16, 64, 196, seed=104, layout="NHWC"),
+                 Case(8, 96, 784, seed=105, layout="NHWC")):
+        d = L.desc(case.N, case.C, case.HW, L.F32, L.NHWC)
+        assert L.query_schedule(d, 0, flag)[0] == 4 and L.query_schedule(d, 1, flag)[0] == 4
+        x, dz, p = inputs(case)
+        ref = _ref(case, x, dz, p, act)
+        for fl in (0, L.VARIANT_I, L.FORCE_STREAMING):
+            errs = _errs(case, _run_gpu(case, x, dz, p, act, flags=fl), ref)
+            assert all(v <= TOL for v in errs.values()), (fl, errs)

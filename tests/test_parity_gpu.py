@@ -127,18 +127,30 @@ def test_fused_and_streaming_agree():
         assert vec_err(to64(a[k]), to64(b[k])) < 1e-5
 
 
-def test_eval_mode():
+@pytest.mark.parametrize("case", [
+    Case(4, 12, 50, seed=10),                              # NCHW rows apply, ragged planes
+    Case(3, 20, 3, seed=11),                               # NCHW HW < V: per-element channel
+    Case(2, 32, 4, seed=12),                               # NCHW aligned small planes
+    Case(4, 64, 49, dtype="bf16", seed=13),                # bf16 straddling vectors
+    Case(4, 64, 50, layout="NHWC", seed=14),               # NHWC fixed channel groups
+    Case(3, 7, 11, layout="NHWC", seed=15),                # NHWC unaligned rows
+    Case(4, 16, 64, gamma_mode="plain", seed=16),          # gamma used as given
+    Case(4, 16, 64, gamma_mode="fixed_one", layout="NHWC", seed=17)],
+    ids=["rows", "hw3", "hw4", "bf16", "nhwc", "nhwc_odd", "plain", "fixed_one"])
+def test_eval_mode(case):
+    """Eval forward in one launch (the apply derives the coefficients from
+    the running statistics, every apply variant) against the oracle's eval forward."""
     import oracle
     import paper_1712_02616_b200 as P
-    case = Case(4, 12, 50, seed=10)
     x, _, p = inputs(case)
-    rm = torch.randn(12) * 0.1
-    rv = torch.rand(12) + 0.5
+    rm = torch.randn(case.C) * 0.1
+    rv = torch.rand(case.C) + 0.5
     z, sm, sv = P.forward(x.cuda(), p.gamma.cuda(), p.beta.cuda(), rm.cuda(), rv.cuda(),
-                          training=False)
+                          training=False, layout=case.layout, gamma_mode=case.gamma_mode)
     assert sm is None and sv is None
-    ref = oracle.load().forward_eval(to64(x), to64(p.gamma), to64(p.beta), to64(rm), to64(rv))
-    assert chan_err(to64(z), ref, 1) < 1e-5
+    ref = oracle.load().forward_eval(to64(x), to64(p.gamma), to64(p.beta), to64(rm), to64(rv),
+                                     layout=case.layout, gamma_mode=case.gamma_mode)
+    assert chan_err(to64(z), ref, case.ax) < (1e-5 if case.dtype == "f32" else 1e-2)
 
 
 # ------------------------------------------------------------------ cfg2 (BASELINE.json configs[1]) full size

@@ -31,12 +31,16 @@ echo measurements-done
 C="python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --sync-emulated 0"
 timeout 300 $C > gpurun_out/fin_plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/fin_launches.csv $C > gpurun_out/fin_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_kernel -s 2 -c 2 -o gpurun_out/fin_fused $C > gpurun_out/fin_ncu_full.log 2>&1
+# gpurun_out must stay under 64 MiB: keep the fused report, summarise the others here
+summ() { [ -f gpurun_out/$1.ncu-rep ] && python tools/ncu_summary.py gpurun_out/$1.ncu-rep > gpurun_out/$1_summary.txt 2>&1 && rm -f gpurun_out/$1.ncu-rep; }
 P1="python tools/layer_probe.py 32 128 196 bf16 NHWC"
-timeout 120 $P1 > gpurun_out/fin_probe1.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:nhwc_fused -s 2 -c 2 -o gpurun_out/fin_nhwc_128x196 $P1 > gpurun_out/fin_ncu_nhwc.log 2>&1
+timeout 120 $P1 > gpurun_out/fin_probe1.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:nhwc_fused -s 2 -c 2 -o gpurun_out/fin_nhwc_128x196 $P1 > gpurun_out/fin_ncu_nhwc.log 2>&1; summ fin_nhwc_128x196
 P2="python tools/layer_probe.py 32 512 196 bf16 NCHW"
-timeout 120 $P2 > gpurun_out/fin_probe2.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:small_kernel -s 2 -c 2 -o gpurun_out/fin_small_512x196 $P2 > gpurun_out/fin_ncu_small.log 2>&1
+timeout 120 $P2 > gpurun_out/fin_probe2.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:small_kernel -s 2 -c 2 -o gpurun_out/fin_small_512x196 $P2 > gpurun_out/fin_ncu_small.log 2>&1; summ fin_small_512x196
 P3="python tools/act_once.py leaky_relu NHWC 32x128x3136 bf16"
-timeout 120 $P3 > gpurun_out/fin_probe3.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"nhwc_bulk_reduce|apply_nhwc" -c 4 -o gpurun_out/fin_nhwc_stream_128x3136 $P3 > gpurun_out/fin_ncu_nhwc_stream.log 2>&1
+timeout 120 $P3 > gpurun_out/fin_probe3.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"nhwc_bulk_reduce|apply_nhwc" -c 4 -o gpurun_out/fin_nhwc_stream_128x3136 $P3 > gpurun_out/fin_ncu_nhwc_stream.log 2>&1; summ fin_nhwc_stream_128x3136
 P4="python tools/act_once.py sigmoid NCHW 32x256x3136"
 timeout 120 $P4 > gpurun_out/fin_probe4.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/fin_act_launches.csv $P4 > gpurun_out/fin_ncu_act.log 2>&1
+python tools/ncu_summary.py gpurun_out/fin_fused.ncu-rep > gpurun_out/fin_fused_summary.txt 2>&1
+du -sh gpurun_out
 echo ncu-done
