@@ -1874,151 +1874,38 @@ iabn_status act_reduce(const Geom& g, int S, const float* z, const float* dz, co
     return check_launch("act_bwd_reduce kernel");
 }
 
-iabn_status act_forward(const Ctx& c, const float* x, float* z, const float* gamma,
-                        const float* beta, float* rm, float* rv, float* sm, float* sv,
-                        float momentum, float eps, uint32_t flags) {
-    if (!(flags & (IABN_EVAL | IABN_FORCE_STREAMING | IABN_FORCE_FUSED))) {  // small NCHW layers
-        const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
-        if (sp.ok) {
-            SmallArgs a{};
-            a.in0 = x;
-            a.out = z;
-            a.gamma = gamma;
-            a.beta = beta;
-            a.running_mean = rm;
-            a.running_var = rv;
-            a.save_mean = sm;
-            a.save_var = sv;
-            a.momentum = momentum;
-            a.eps = eps;
-            a.slope = 1.f;
-            a.inv_slope = 1.f;
-            a.flags = flags;
-            return (flags & IABN_ACT_SIGMOID) ? launch_small<float, 1>(0, c.g, sp, a, c.st)
-                                              : launch_small<float, 2>(0, c.g, sp, a, c.st);
-        }
-    }
-    if (!(flags & (IABN_EVAL | IABN_FORCE_STREAMING))) {  // NCHW: the channel-resident kernels
-        const FusedPlan p = fused_plan(c.g, 0, *c.dev, flags);
-        if (p.ok) {
-            const FusedArgs a = fused_fwd_args(c.g, x, z, gamma, beta, rm, rv, sm, sv, momentum,
-                                               eps, 1.f, flags);
-            return (flags & IABN_ACT_SIGMOID) ? launch_fused<float, 1>(0, p, a, c.st)
-                                              : launch_fused<float, 2>(0, p, a, c.st);
-        }
-        const NhwcPlan np = nhwc_plan(c.g, 0, *c.dev, flags);  // NHWC: channel groups
-        if (np.ok) {
-            NhwcArgs a{};
-            a.gamma = gamma;
-            a.beta = beta;
-            a.running_mean = rm;
-            a.running_var = rv;
-            a.save_mean = sm;
-            a.save_var = sv;
-            a.momentum = momentum;
-            a.eps = eps;
-            a.slope = 1.f;
-            a.inv_slope = 1.f;
-            a.flags = flags;
-            return (flags & IABN_ACT_SIGMOID) ? launch_nhwc<float, 1>(0, c.g, np, a, x, nullptr, z, c.st)
-                                              : launch_nhwc<float, 2>(0, c.g, np, a, x, nullptr, z, c.st);
-        }
-    }
-    float4* coef = wsp<float4>(c, c.w.coef);
-    if (flags & IABN_EVAL) {
-        launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv, eps, flags, coef);
-        IABN_TRY(check_launch("eval_coef kernel"));
-    } else {
-        IABN_TRY(launch_stats<float>(c.g, c.S, x, wsp<double>(c, c.w.part), c.st));
-        FwdCoefArgs a{wsp<double>(c, c.w.part), c.S, c.g.C, gamma, beta, rm, rv, sm, sv, coef,
-                      momentum, eps, flags};
-        launch_pdl(fwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
-        IABN_TRY(check_launch("fwd_coef kernel"));
-    }
-    return (flags & IABN_ACT_SIGMOID)
-               ? act_elementwise<1>(c.g, 0, x, nullptr, z, coef, c.dev->sms, c.st)
-               : act_elementwise<2>(c.g, 0, x, nullptr, z, coef, c.dev->sms, c.st);
-}
-
-iabn_status act_backward(const Ctx& c, const float* z, const float* dz, float* dx,
-                         const float* gamma, const float* beta, const float* sv, float* dg,
-                         float* db, float eps, uint32_t flags) {
-    const bool sig = flags & IABN_ACT_SIGMOID;
-    if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED))) {  // small NCHW layers
-        const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
-        if (sp.ok) {
-            SmallArgs a{};
-            a.in0 = z;
-            a.in1 = dz;
-            a.out = dx;
-            a.gamma = gamma;
-            a.beta = beta;
-            a.save_var = const_cast<float*>(sv);
-            a.dgamma = dg;
-            a.dbeta = db;
-            a.eps = eps;
-            a.slope = 1.f;
-            a.inv_slope = 1.f;
-            a.flags = flags;
-            return sig ? launch_small<float, 1>(1, c.g, sp, a, c.st) : launch_small<float, 2>(1, c.g, sp, a, c.st);
-        }
-    }
-    if (!(flags & IABN_FORCE_STREAMING)) {
-        const FusedPlan p = fused_plan(c.g, 1, *c.dev, flags);
-        if (p.ok) {
-            const FusedArgs a = fused_bwd_args(c.g, z, dz, dx, gamma, beta, sv, dg, db, eps, 1.f,
-                                               flags);
-            return sig ? launch_fused<float, 1>(1, p, a, c.st) : launch_fused<float, 2>(1, p, a, c.st);
-        }
-        const NhwcPlan np = nhwc_plan(c.g, 1, *c.dev, flags);  // NHWC: channel groups
-        if (np.ok) {
-            NhwcArgs a{};
-            a.gamma = gamma;
-            a.beta = beta;
-            a.save_var = const_cast<float*>(sv);
-            a.dgamma = dg;
-            a.dbeta = db;
-            a.eps = eps;
-            a.slope = 1.f;
-            a.inv_slope = 1.f;
-            a.flags = flags;
-            return sig ? launch_nhwc<float, 1>(1, c.g, np, a, z, dz, dx, c.st)
-                       : launch_nhwc<float, 2>(1, c.g, np, a, z, dz, dx, c.st);
-        }
-    }
-    double* part = wsp<double>(c, c.w.part);
-    float4* coef = wsp<float4>(c, c.w.coef);
-    // NHWC: the bulk-ring reduction when it applies (c.S = its cluster records), else the
-    // LDG splits within the workspace's 296 records
-    int S = c.S;
-    if (c.g.layout == IABN_NHWC && nb_grid(c.g)) {
-        const iabn_status st = sig ? launch_nb<float, 1, 1>(c.g, S, z, dz, gamma, beta, eps, 1.f, flags, part, c.st)
-                                   : launch_nb<float, 1, 2>(c.g, S, z, dz, gamma, beta, eps, 1.f, flags, part, c.st);
-        IABN_TRY(st);
-    } else {
-        if (c.g.layout == IABN_NHWC) S = (int)std::min<int64_t>(stat_splits_ldg(c.g), kGresMaxG);
-        IABN_TRY(sig ? act_reduce<1>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st)
-                     : act_reduce<2>(c.g, S, z, dz, gamma, beta, eps, flags, part, c.st));
-    }
-    BwdCoefArgs a{part, S, part, S, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg, db,
-                  coef, eps, flags};
+template <typename T>
+iabn_status bwd_from_sums(const Ctx& c, const double* glob, int Sg, const double* loc, int Sl,
+                          const double* count_ptr, double count, const void* z, const void* dz,
+                          void* dx, const float* gamma, const float* beta, const float* sv,
+                          float* dg, float* db, float eps, float slope, uint32_t flags) {
+    BwdCoefArgs a{glob, Sg, loc, Sl, count_ptr, count, c.g.C, gamma, beta, sv, dg, db,
+                  wsp<float4>(c, c.w.coef), eps, flags};
     launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
     IABN_TRY(check_launch("bwd_coef kernel"));
-    return sig ? act_elementwise<1>(c.g, 1, z, dz, dx, coef, c.dev->sms, c.st)
-               : act_elementwise<2>(c.g, 1, z, dz, dx, coef, c.dev->sms, c.st);
+    return launch_bwd_apply<T>(c.g, z, dz, dx, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
 }
 
-template <typename T>
-iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamma,
-                         const float* beta, float* rm, float* rv, float* sm, float* sv,
-                         float momentum, float eps, float slope, uint32_t flags) {
-    if constexpr (std::is_same<T, float>::value)
-        if (act_of(flags))
-            return act_forward(c, (const float*)x, (float*)z, gamma, beta, rm, rv, sm, sv,
-                               momentum, eps, flags);
-    if (flags & IABN_EVAL)  // one launch: the apply derives its coefficients (EvalCoef)
-        return launch_fwd_apply_ev<T, true>(c.g, x, z, nullptr, slope, c.dev->sms, c.st,
-                                             EvalCoef{gamma, beta, rm, rv, eps, flags});
+// One dispatch for every activation (ACT 0 leaky ReLU, 1 sigmoid, 2 tanh; ACT != 0 only
+// with T = float): register-resident small layers -> channel-resident clusters (NCHW) ->
+// channel groups (NHWC) -> [leaky: grid-resident NHWC, opt-in] -> streaming.
+template <typename T, int ACT>
+iabn_status forward_sched(const Ctx& c, const void* x, void* z, const float* gamma,
+                          const float* beta, float* rm, float* rv, float* sm, float* sv,
+                          float momentum, float eps, float slope, uint32_t flags) {
+    if (flags & IABN_EVAL) {
+        if constexpr (ACT == 0) {  // one launch: the apply derives its coefficients (EvalCoef)
+            return launch_fwd_apply_ev<T, true>(c.g, x, z, nullptr, slope, c.dev->sms, c.st,
+                                                 EvalCoef{gamma, beta, rm, rv, eps, flags});
+        } else {
+            float4* coef = wsp<float4>(c, c.w.coef);
+            launch_pdl(eval_coef_kernel, cgrid(c.g.C), 128, 0, c.st, c.g.C, gamma, beta, rm, rv,
+                       eps, flags, coef);
+            IABN_TRY(check_launch("eval_coef kernel"));
+            return act_elementwise<ACT>(c.g, 0, (const float*)x, nullptr, (float*)z, coef,
+                                        c.dev->sms, c.st);
+        }
+    }
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
         const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
         if (sp.ok) {
@@ -2036,7 +1923,7 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
             a.slope = slope;
             a.inv_slope = 1.0f / slope;
             a.flags = flags;
-            return launch_small<T>(0, c.g, sp, a, c.st);
+            return launch_small<T, ACT>(0, c.g, sp, a, c.st);
         }
     }
     FusedPlan p;
@@ -2044,10 +1931,10 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
     if ((flags & IABN_FORCE_FUSED) && !p.ok && c.g.layout != IABN_NHWC)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident forward not possible for this shape");
     if (p.ok)
-        return launch_fused<T>(0, p,
-                               fused_fwd_args(c.g, x, z, gamma, beta, rm, rv, sm, sv, momentum, eps,
-                                              slope, flags),
-                               c.st);
+        return launch_fused<T, ACT>(0, p,
+                                    fused_fwd_args(c.g, x, z, gamma, beta, rm, rv, sm, sv,
+                                                   momentum, eps, slope, flags),
+                                    c.st);
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_RESIDENT))) {
         const NhwcPlan np = nhwc_plan(c.g, 0, *c.dev, flags);
         if (np.ok) {
@@ -2063,53 +1950,49 @@ iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamm
             a.slope = slope;
             a.inv_slope = 1.0f / slope;
             a.flags = flags;
-            return launch_nhwc<T>(0, c.g, np, a, x, nullptr, z, c.st);
+            return launch_nhwc<T, ACT>(0, c.g, np, a, x, nullptr, z, c.st);
         }
         if (flags & IABN_FORCE_FUSED)
             return fail(IABN_ERR_UNSUPPORTED, "channel-group NHWC forward not possible for this shape");
     }
-    if (const int G = gres_grid(c.g, 0, flags, *c.dev)) {
-        GresArgs a{};
-        a.in0 = x;
-        a.out = z;
-        a.C = c.g.C;
-        a.rows = c.g.m;
-        a.cv = (uint32_t)(c.g.C * c.g.b / 16);
-        a.slope = slope;
-        a.inv_slope = 1.0f / slope;
-        a.eps = eps;
-        a.flags = flags;
-        a.part = wsp<double>(c, c.w.part);
-        a.coef = wsp<float4>(c, c.w.coef);
-        a.fwd = FwdCoefArgs{a.part, G, c.g.C, gamma, beta, rm, rv, sm, sv, a.coef, momentum, eps,
-                            flags};
-        return launch_gres<T, 0>(c.g, G, a, c.st);
+    if constexpr (ACT == 0) {
+        if (const int G = gres_grid(c.g, 0, flags, *c.dev)) {
+            GresArgs a{};
+            a.in0 = x;
+            a.out = z;
+            a.C = c.g.C;
+            a.rows = c.g.m;
+            a.cv = (uint32_t)(c.g.C * c.g.b / 16);
+            a.slope = slope;
+            a.inv_slope = 1.0f / slope;
+            a.eps = eps;
+            a.flags = flags;
+            a.part = wsp<double>(c, c.w.part);
+            a.coef = wsp<float4>(c, c.w.coef);
+            a.fwd = FwdCoefArgs{a.part, G, c.g.C, gamma, beta, rm, rv, sm, sv, a.coef, momentum,
+                                eps, flags};
+            return launch_gres<T, 0>(c.g, G, a, c.st);
+        }
     }
     IABN_TRY(fwd_stream_stats<T>(c, x));
-    return fwd_from_partials<T>(c, wsp<double>(c, c.w.part), c.S, x, z, gamma, beta, rm, rv, sm,
-                                sv, momentum, eps, slope, flags);
+    if constexpr (ACT == 0) {
+        return fwd_from_partials<T>(c, wsp<double>(c, c.w.part), c.S, x, z, gamma, beta, rm, rv,
+                                    sm, sv, momentum, eps, slope, flags);
+    } else {
+        float4* coef = wsp<float4>(c, c.w.coef);
+        FwdCoefArgs a{wsp<double>(c, c.w.part), c.S, c.g.C, gamma, beta, rm, rv, sm, sv, coef,
+                      momentum, eps, flags};
+        launch_pdl(fwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
+        IABN_TRY(check_launch("fwd_coef kernel"));
+        return act_elementwise<ACT>(c.g, 0, (const float*)x, nullptr, (float*)z, coef,
+                                    c.dev->sms, c.st);
+    }
 }
 
-template <typename T>
-iabn_status bwd_from_sums(const Ctx& c, const double* glob, int Sg, const double* loc, int Sl,
-                          const double* count_ptr, double count, const void* z, const void* dz,
-                          void* dx, const float* gamma, const float* beta, const float* sv,
-                          float* dg, float* db, float eps, float slope, uint32_t flags) {
-    BwdCoefArgs a{glob, Sg, loc, Sl, count_ptr, count, c.g.C, gamma, beta, sv, dg, db,
-                  wsp<float4>(c, c.w.coef), eps, flags};
-    launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
-    IABN_TRY(check_launch("bwd_coef kernel"));
-    return launch_bwd_apply<T>(c.g, z, dz, dx, wsp<float4>(c, c.w.coef), slope, c.dev->sms, c.st);
-}
-
-template <typename T>
-iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
-                          const float* gamma, const float* beta, const float* sv, float* dg,
-                          float* db, float eps, float slope, uint32_t flags) {
-    if constexpr (std::is_same<T, float>::value)
-        if (act_of(flags))
-            return act_backward(c, (const float*)z, (const float*)dz, (float*)dx, gamma, beta, sv,
-                                dg, db, eps, flags);
+template <typename T, int ACT>
+iabn_status backward_sched(const Ctx& c, const void* z, const void* dz, void* dx,
+                           const float* gamma, const float* beta, const float* sv, float* dg,
+                           float* db, float eps, float slope, uint32_t flags) {
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_FUSED | IABN_FORCE_RESIDENT))) {
         const SmallPlan sp = small_plan(c.g, flags, c.dev->sms);
         if (sp.ok) {
@@ -2126,7 +2009,7 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
             a.slope = slope;
             a.inv_slope = 1.0f / slope;
             a.flags = flags;
-            return launch_small<T>(1, c.g, sp, a, c.st);
+            return launch_small<T, ACT>(1, c.g, sp, a, c.st);
         }
     }
     FusedPlan p;
@@ -2134,10 +2017,10 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
     if ((flags & IABN_FORCE_FUSED) && !p.ok && c.g.layout != IABN_NHWC)
         return fail(IABN_ERR_UNSUPPORTED, "channel-resident backward not possible for this shape");
     if (p.ok)
-        return launch_fused<T>(1, p,
-                               fused_bwd_args(c.g, z, dz, dx, gamma, beta, sv, dg, db, eps, slope,
-                                              flags),
-                               c.st);
+        return launch_fused<T, ACT>(1, p,
+                                    fused_bwd_args(c.g, z, dz, dx, gamma, beta, sv, dg, db, eps,
+                                                   slope, flags),
+                                    c.st);
     if (!(flags & (IABN_FORCE_STREAMING | IABN_FORCE_RESIDENT))) {
         const NhwcPlan np = nhwc_plan(c.g, 1, *c.dev, flags);
         if (np.ok) {
@@ -2151,35 +2034,85 @@ iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
             a.slope = slope;
             a.inv_slope = 1.0f / slope;
             a.flags = flags;
-            return launch_nhwc<T>(1, c.g, np, a, z, dz, dx, c.st);
+            return launch_nhwc<T, ACT>(1, c.g, np, a, z, dz, dx, c.st);
         }
         if (flags & IABN_FORCE_FUSED)
             return fail(IABN_ERR_UNSUPPORTED, "channel-group NHWC backward not possible for this shape");
     }
     double* part = wsp<double>(c, c.w.part);
-    if (const int G = gres_grid(c.g, 1, flags, *c.dev)) {
-        GresArgs a{};
-        a.in0 = z;
-        a.in1 = dz;
-        a.out = dx;
-        a.C = c.g.C;
-        a.rows = c.g.m;
-        a.cv = (uint32_t)(c.g.C * c.g.b / 16);
-        a.slope = slope;
-        a.inv_slope = 1.0f / slope;
-        a.eps = eps;
-        a.flags = flags;
-        a.gamma = gamma;
-        a.beta = beta;
-        a.part = part;
-        a.coef = wsp<float4>(c, c.w.coef);
-        a.bwd = BwdCoefArgs{part, G, part, G, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg,
-                            db, a.coef, eps, flags};
-        return launch_gres<T, 1>(c.g, G, a, c.st);
+    if constexpr (ACT == 0) {
+        if (const int G = gres_grid(c.g, 1, flags, *c.dev)) {
+            GresArgs a{};
+            a.in0 = z;
+            a.in1 = dz;
+            a.out = dx;
+            a.C = c.g.C;
+            a.rows = c.g.m;
+            a.cv = (uint32_t)(c.g.C * c.g.b / 16);
+            a.slope = slope;
+            a.inv_slope = 1.0f / slope;
+            a.eps = eps;
+            a.flags = flags;
+            a.gamma = gamma;
+            a.beta = beta;
+            a.part = part;
+            a.coef = wsp<float4>(c, c.w.coef);
+            a.bwd = BwdCoefArgs{part, G, part, G, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv,
+                                dg, db, a.coef, eps, flags};
+            return launch_gres<T, 1>(c.g, G, a, c.st);
+        }
+        IABN_TRY(launch_bwd_reduce<T>(c.g, c.S, z, dz, gamma, beta, eps, slope, flags, part, c.st));
+        return bwd_from_sums<T>(c, part, c.S, part, c.S, nullptr, (double)c.g.m, z, dz, dx, gamma,
+                                beta, sv, dg, db, eps, slope, flags);
+    } else {
+        // NHWC: the bulk-ring reduction when it applies (c.S = its cluster records), else
+        // the LDG act reductions (NHWC: within the workspace's 296 records)
+        int S = c.S;
+        if (c.g.layout == IABN_NHWC && nb_grid(c.g)) {
+            const iabn_status st = launch_nb<float, 1, ACT>(c.g, S, z, dz, gamma, beta, eps, 1.f,
+                                                            flags, part, c.st);
+            IABN_TRY(st);
+        } else {
+            if (c.g.layout == IABN_NHWC) S = (int)std::min<int64_t>(stat_splits_ldg(c.g), kGresMaxG);
+            IABN_TRY(act_reduce<ACT>(c.g, S, (const float*)z, (const float*)dz, gamma, beta, eps,
+                                     flags, part, c.st));
+        }
+        float4* coef = wsp<float4>(c, c.w.coef);
+        BwdCoefArgs a{part, S, part, S, nullptr, (double)c.g.m, c.g.C, gamma, beta, sv, dg, db,
+                      coef, eps, flags};
+        launch_pdl(bwd_coef_kernel, wgrid(c.g.C), 128, 0, c.st, a);
+        IABN_TRY(check_launch("bwd_coef kernel"));
+        return act_elementwise<ACT>(c.g, 1, (const float*)z, (const float*)dz, (float*)dx, coef,
+                                    c.dev->sms, c.st);
     }
-    IABN_TRY(launch_bwd_reduce<T>(c.g, c.S, z, dz, gamma, beta, eps, slope, flags, part, c.st));
-    return bwd_from_sums<T>(c, part, c.S, part, c.S, nullptr, (double)c.g.m, z, dz, dx, gamma,
-                            beta, sv, dg, db, eps, slope, flags);
+}
+
+// sigmoid / tanh take slope = 1 (unused by their kernels) and fp32 storage only
+// (check_act_flags rejects bf16 before any launch)
+template <typename T>
+iabn_status forward_impl(const Ctx& c, const void* x, void* z, const float* gamma,
+                         const float* beta, float* rm, float* rv, float* sm, float* sv,
+                         float momentum, float eps, float slope, uint32_t flags) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (flags & IABN_ACT_SIGMOID)
+            return forward_sched<T, 1>(c, x, z, gamma, beta, rm, rv, sm, sv, momentum, eps, 1.f, flags);
+        if (flags & IABN_ACT_TANH)
+            return forward_sched<T, 2>(c, x, z, gamma, beta, rm, rv, sm, sv, momentum, eps, 1.f, flags);
+    }
+    return forward_sched<T, 0>(c, x, z, gamma, beta, rm, rv, sm, sv, momentum, eps, slope, flags);
+}
+
+template <typename T>
+iabn_status backward_impl(const Ctx& c, const void* z, const void* dz, void* dx,
+                          const float* gamma, const float* beta, const float* sv, float* dg,
+                          float* db, float eps, float slope, uint32_t flags) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (flags & IABN_ACT_SIGMOID)
+            return backward_sched<T, 1>(c, z, dz, dx, gamma, beta, sv, dg, db, eps, 1.f, flags);
+        if (flags & IABN_ACT_TANH)
+            return backward_sched<T, 2>(c, z, dz, dx, gamma, beta, sv, dg, db, eps, 1.f, flags);
+    }
+    return backward_sched<T, 0>(c, z, dz, dx, gamma, beta, sv, dg, db, eps, slope, flags);
 }
 
 // ====================================================================== fault injection
