@@ -4,19 +4,21 @@
 // on chip).  Its reductions (F1 statistics, B1 gradient sums) were LDG loops whose CTAs
 // each covered ~256 rows with 2-4 rows in flight per thread; ncu on DenseNet's
 // 128x56^2 bf16 layer: 1.4 TB/s (statistics) and 1.7 TB/s (gradient sums).  Here CTA s
-// of a grid of G (<= 2 per SM) takes the chunks s, s + G, ... of rps whole rows (at any
-// moment the grid reads one contiguous front of the tensor) and streams them through a
-// 4-stage shared-memory ring with cp.async.bulk (one elected thread, mbarrier
-// complete_tx), 64 KB in flight per CTA whatever the register budget.  Consumers read 16-byte vectors from the ring:
+// of a grid of G <= 256 (32 clusters of 8 at 2 CTAs per SM: all resident at once) takes
+// the chunks s, s + G, ... of rps whole rows (at any moment the grid reads one contiguous
+// front of the tensor) and streams them through a 4-stage shared-memory ring with
+// cp.async.bulk (one elected thread, mbarrier complete_tx), 64 KB in flight per CTA
+// whatever the register budget.  Consumers read 16-byte vectors from the ring:
 //   cv = C*b/16 <= 256 vectors per row; blockDim = rt * cv (rt = 256 / cv row lanes):
 //   thread t takes vector j = t % cv (channels j*V .. j*V + V-1) of rows t / cv, + rt, ...
 // Packed fp32x2 (FADD2 / FFMA2) and bf16x2 (FHADD / FHFMA.BF16) arithmetic, fp32 per
 // thread in runs of <= 64 rows, fp64 across runs; then the rt row lanes in a fixed order
 // in shared memory, and the 8 CTAs of a cluster in rank order over DSMEM -> one record
 // per (cluster, channel): F1 raw moments (count, sum, sum of squares, shifted by the
-// channel's first value as everywhere, R8) or B1 (sum dy, sum dy x^) -- the
-// record layout the coefficient kernels combine (37 records instead of 296).  Requires
-// C*b % 16 == 0 (bulk copies of whole rows) and C*b <= 4 KB.
+// channel's first value as everywhere, R8) or B1 -- (sum dz, sum_{z<0} dz,
+// sum dz z) folded to (S1, S2) by BN-dagger, or (sum dy, sum dy x^) with IABN_VARIANT_I --
+// the record layout the coefficient kernels combine (<= 32 records instead of 296).
+// Requires C*b % 16 == 0 (bulk copies of whole rows) and C*b <= 4 KB.
 #pragma once
 
 #include "common.cuh"
