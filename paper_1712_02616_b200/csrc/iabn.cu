@@ -794,7 +794,7 @@ std::atomic<int> g_nhwc_force_g{0}, g_nhwc_force_k{0}, g_nhwc_force_clusters{0};
 // 2-D TMA boxes of narrow rows move few bytes per request, so the per-CTA chain (load,
 // reduce, exchange, apply, store) is short only for small slabs and many CTAs: group rows
 // of 32 bytes (then 64, then 16), K = ceil(128 / groups) CTAs per group (at least 128 CTAs
-// when the channels allow, at most 8 per cluster), raised while a backward CTA would hold
+// when the channels allow; ~96 for <= 16 groups; at most 8 per cluster), raised while a backward CTA would hold
 // more than 80 KB, all groups in one wave of co-resident clusters.  Layers with more than
 // 32768 rows (N*HW; the 56x56 and 112x112 layers at N = 32) keep the streaming schedule:
 // their groups do not fit on chip at a useful width.  Env IABN_NHWC_G (channels) /
@@ -874,7 +874,10 @@ NhwcPlan nhwc_plan(const Geom& g, int pass, const DevFacts& f, uint32_t flags) {
     for (const int gb : {32, 64, 16}) {
         if (gb / g.b > g.C && gb > 16) continue;
         const int64_t groups = (g.C * g.b + gb - 1) / gb;
-        int K = (int)std::min<int64_t>(kNhwcMaxK, std::max<int64_t>(1, (128 + groups - 1) / groups));
+        // ~128 CTAs; ~96 when the groups are few (<= 16: K = 6 at 16 groups measured 8-12 %
+        // faster than 8, r02: bf16 256x14^2 18.5 -> 16.4 us, fp32 128x14^2 16.0 -> 14.2 us)
+        const int64_t tgt = groups <= 16 ? (96 + groups / 2) / groups : (128 + groups - 1) / groups;
+        int K = (int)std::min<int64_t>(kNhwcMaxK, std::max<int64_t>(1, tgt));
         NhwcPlan p;
         for (; K <= kNhwcMaxK; ++K) {  // the first one-wave plan from the target K up
             p = make(gb, K);
