@@ -31,6 +31,9 @@ constexpr int kSmallThreads = 256;
 #ifndef IABN_SMALL_MINB_F4
 #define IABN_SMALL_MINB_F4 4  // forward, R = 4: CTAs per SM the register cap is sized for
 #endif
+#ifndef IABN_SMALL_MINB_B4
+#define IABN_SMALL_MINB_B4 4  // backward, R = 4 (64 registers: spills ~70 bytes of stack)
+#endif
 constexpr int kSmallR = 8;  // most 16-byte slots per thread and input (R = 4 or 8)
 
 struct SmallArgs {
@@ -75,7 +78,7 @@ __device__ __forceinline__ uint4 ldg_coherent(const void* p) {
 
 // ACT: 0 leaky ReLU, 1 sigmoid, 2 tanh (fp32 only; kernels_act.cuh)
 template <typename T, int PASS, int R, int ACT = 0>
-__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMALL_MINB_F4 : 4) : (PASS == 0 ? 3 : 2))
+__global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMALL_MINB_F4 : IABN_SMALL_MINB_B4) : (PASS == 0 ? 3 : 2))
     small_kernel(const SmallArgs a) {
     constexpr int V = Elem<T>::kVec;
     constexpr int NP = Pairs<T>::kN;
