@@ -31,6 +31,9 @@ constexpr int kSmallThreads = 256;
 #ifndef IABN_SMALL_MINB_F4
 #define IABN_SMALL_MINB_F4 4  // forward, R = 4: CTAs per SM the register cap is sized for
 #endif
+#ifndef IABN_SMALL_L2HINT
+#define IABN_SMALL_L2HINT ""  // experiments: ".L2::128B" / ".L2::256B" prefetch-size hint
+#endif
 #ifndef IABN_SMALL_MINB_B4
 #define IABN_SMALL_MINB_B4 4  // backward, R = 4 (64 registers: spills ~70 bytes of stack)
 #endif
@@ -70,7 +73,7 @@ __device__ __forceinline__ bool mis_valid_small(uint32_t i, int k, uint32_t h, u
 
 __device__ __forceinline__ uint4 ldg_coherent(const void* p) {
     uint4 r;
-    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+    asm volatile("ld.global.L1::no_allocate" IABN_SMALL_L2HINT ".v4.u32 {%0, %1, %2, %3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
