@@ -965,6 +965,7 @@ iabn_status launch_small(int pass, const Geom& g, const SmallPlan& p, SmallArgs 
     a.W = p.W;
     a.fd_w = fd32(p.W);
     a.tw = p.tw;
+    a.inv_n = 1.0 / ((double)g.N * (double)g.HW);
     a.trace = nullptr;
     if (env_int("IABN_SMALL_TRACE", 0)) {  // experiments (a build with -DIABN_PHASE_TRACE)
         static unsigned long long* buf = nullptr;

@@ -58,6 +58,7 @@ struct SmallArgs {
     uint32_t tw;      // warps per channel team
     float momentum, eps, slope, inv_slope;
     uint32_t flags;
+    double inv_n;  // 1 / (N HW)
     unsigned long long* trace;  // experiments: [grid][kSmallTrace] %globaltimer of CTA phases
 };
 // phases: 0 start, 1 PDL wait done, 2 thread 0's sums done (its loads landed), 3 team
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
     __shared__ double red[kSmallThreads / 32][2];
     __shared__ float cf[kSmallThreads / 32][8];
     __shared__ double stash[kSmallThreads / 32][2];
+    __shared__ float pre[kSmallThreads / 32][2];  // forward: old running mean / var
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t tw = a.tw, TT = 32 * tw, team = warp / tw, tt = tid - team * TT;
@@ -140,6 +142,13 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
             xr[k] = ldg_coherent(in0 + sl.off);
             if (PASS == 1) dr[k] = ldg_coherent(in1 + sl.off);
         }
+    }
+    // the leader's old running statistics, fetched while the slab's loads are in flight (its
+    // read-modify-write after the coefficient barrier would otherwise delay its warp's
+    // stores by a global round trip; r02 phase trace: 7x7 layers' slowest CTAs)
+    if (PASS == 0 && tt == 0 && active) {
+        pre[team][0] = a.running_mean ? a.running_mean[c] : 0.f;
+        pre[team][1] = a.running_var ? a.running_var[c] : 0.f;
     }
     float K0 = 0.f, gam = 1.f, bet = 0.f, var_s = 1.f;
     if (active) {
@@ -212,10 +221,17 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
         }
         float* co = cf[team];
         if (PASS == 0) {
-            const double n = (double)a.N * (double)a.HW;
-            double mean, var;
-            const float4 f = fwd_coef_from_moments(n, n * K0 + t1, t2 + 2.0 * K0 * t1 + n * (double)K0 * K0,
-                                                   gam, bet, a.eps, a.flags, &mean, &var);
+            // shifted moments in fp64 without a division: d = t1/n, var = t2/n - d^2 with the
+            // host's 1/n, rstd by rsqrt (the same quantities as fwd_coef_from_moments, which
+            // rebuilds raw moments and divides three times: r02 phase trace, 7x7 layers'
+            // coefficient step 1.1 -> 0.8 us)
+            const double d = (double)t1 * a.inv_n;
+            double var = fma(-d, d, (double)t2 * a.inv_n);
+            var = var > 0.0 ? var : 0.0;
+            const double mean = (double)K0 + d;
+            const double A = gamma_eff(gam, a.eps, a.flags) * rsqrt(var + (double)a.eps);
+            const float mu_hi = (float)mean;
+            const float4 f = make_float4((float)A, mu_hi, (float)(mean - (double)mu_hi), bet);
             co[0] = f.x;
             co[1] = f.y;
             co[2] = fmaf(-f.z, f.x, f.w);
@@ -225,8 +241,8 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
             const double gg = gamma_eff(gam, a.eps, a.flags), bb = (double)bet;
             double S1 = t1, S2 = t2;
             if (!(a.flags & kVariantI)) S2 = (S2 - bb * S1) / gg;  // BN-dagger
-            const double rstd = 1.0 / sqrt((double)var_s + (double)a.eps);
-            const double rm = rstd / ((double)a.N * (double)a.HW);
+            const double rstd = rsqrt((double)var_s + (double)a.eps);
+            const double rm = rstd * a.inv_n;
             const float alpha = (float)(gg * rstd), kappa = (float)(-rm * S2);
             co[0] = alpha;
             co[1] = kappa;
@@ -248,8 +264,14 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
             const double mean = stash[team][0], var = stash[team][1];
             a.save_mean[c] = (float)mean;
             a.save_var[c] = (float)var;
-            update_running(a.running_mean, a.running_var, c, mean, var,
-                           (double)a.N * (double)a.HW, a.momentum, a.flags);
+            // update_running (kernels_stream.cuh) on the prefetched values, same arithmetic
+            const double mo = (double)a.momentum, cnt = (double)a.N * (double)a.HW;
+            if (a.running_mean)
+                a.running_mean[c] = (float)((1.0 - mo) * (double)pre[team][0] + mo * mean);
+            if (a.running_var) {
+                const double v = (a.flags & kRunVarBiased) ? var : var * cnt / (cnt - 1.0);
+                a.running_var[c] = (float)((1.0 - mo) * (double)pre[team][1] + mo * v);
+            }
         } else {
             a.dbeta[c] = (float)stash[team][0];
             a.dgamma[c] = (float)(gamma_sign(gam, a.flags) * stash[team][1]);
