@@ -1037,6 +1037,7 @@ iabn_status launch_nhwc(int pass, const Geom& g, const NhwcPlan& p, NhwcArgs a, 
     a.in0 = in0;
     a.C = g.C;
     a.m = (uint32_t)g.m;
+    a.inv_m = 1.0 / (double)g.m;
     a.g = p.g;
     a.cols = p.cols;
     a.ngroups = p.ngroups;

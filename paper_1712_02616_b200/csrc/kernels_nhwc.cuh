@@ -53,6 +53,7 @@ struct NhwcArgs {
     float* dbeta;
     int64_t C;
     uint32_t m;         // rows (N*HW)
+    double inv_m;       // 1 / m
     uint32_t g;         // channels per group
     uint32_t cols;      // 16-byte columns per group row (g*b/16; a power of 2 <= 32)
     uint32_t ngroups;   // ceil(C / g)
@@ -410,9 +411,14 @@ __global__ void __launch_bounds__(kNhwcThreads, 1)
             float* cf = coef + tid * 8;
             if (c < a.C) {
                 if (PASS == 0) {
-                    double mean, var;
-                    const float4 f = fwd_coef_from_moments(tot[0], tot[1], tot[2], pgam[tid],
-                                                           pbet[tid], a.eps, a.flags, &mean, &var);
+                    // fwd_coef_from_moments without its three divisions: the count is the
+                    // layer's m (no sync here), 1/m from the host, rstd by rsqrt
+                    const double mean = tot[1] * a.inv_m;
+                    double var = fma(-mean, mean, tot[2] * a.inv_m);
+                    var = var > 0.0 ? var : 0.0;
+                    const double Ad = gamma_eff(pgam[tid], a.eps, a.flags) * rsqrt(var + (double)a.eps);
+                    const float mu_hi = (float)mean;
+                    const float4 f = make_float4((float)Ad, mu_hi, (float)(mean - (double)mu_hi), pbet[tid]);
                     // y = (x - mu_hi) A + (beta - mu_lo A)
                     cf[0] = f.x;
                     cf[1] = f.y;
@@ -435,8 +441,8 @@ __global__ void __launch_bounds__(kNhwcThreads, 1)
                     const double bet = (double)pbet[tid];
                     double S1 = tot[0], S2 = tot[1];
                     if (!(a.flags & kVariantI)) S2 = (S2 - bet * S1) / gg;  // BN-dagger
-                    const double rstd = 1.0 / sqrt((double)pvar[tid] + (double)a.eps);
-                    const double rm = rstd / (double)a.m;
+                    const double rstd = rsqrt((double)pvar[tid] + (double)a.eps);
+                    const double rm = rstd * a.inv_m;
                     const float alpha = (float)(gg * rstd);
                     const float kappa = (float)(-rm * S2);
                     const float cc = (float)(rm * fma(S2, bet, -gg * S1));
