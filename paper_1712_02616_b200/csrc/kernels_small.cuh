@@ -31,6 +31,9 @@ constexpr int kSmallThreads = 256;
 #ifndef IABN_SMALL_MINB_F4
 #define IABN_SMALL_MINB_F4 4  // forward, R = 4: CTAs per SM the register cap is sized for
 #endif
+#ifndef IABN_SMALL_EARLY_TRIGGER
+#define IABN_SMALL_EARLY_TRIGGER 0
+#endif
 #ifndef IABN_SMALL_L2HINT
 #define IABN_SMALL_L2HINT ""  // experiments: ".L2::128B" / ".L2::256B" prefetch-size hint
 #endif
@@ -114,6 +117,9 @@ __global__ void __launch_bounds__(kSmallThreads, R <= 4 ? (PASS == 0 ? IABN_SMAL
     };
     trace(0);
     pdl_wait();
+#if IABN_SMALL_EARLY_TRIGGER  // experiments: let the next kernel's CTAs launch as ours exit
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     trace(1);
     // slot k of this thread: plane n = i / W, slot si = i % W of the plane's covering
     // range (recomputed where needed: registers go to the data)
