@@ -222,7 +222,7 @@ def test_act_rejections_and_schedule():
 def test_act_nhwc_channel_groups(act):
     """NHWC layers whose channel groups fit on chip take the channel-group kernels with the
     activation as a template parameter (schedule 4); against the oracle with both
-    variants, and against the streaming schedule's result."""
+    variants, and the streaming schedule (bulk-ring reduction with f: both variants)."""
     from paper_1712_02616_b200 import _lib as L
     flag = L.ACT_SIGMOID if act == "sigmoid" else L.ACT_TANH
     for case in (Case(16, 64, 196, seed=104, layout="NHWC"),
@@ -231,6 +231,6 @@ def test_act_nhwc_channel_groups(act):
         assert L.query_schedule(d, 0, flag)[0] == 4 and L.query_schedule(d, 1, flag)[0] == 4
         x, dz, p = inputs(case)
         ref = _ref(case, x, dz, p, act)
-        for fl in (0, L.VARIANT_I, L.FORCE_STREAMING):
+        for fl in (0, L.VARIANT_I, L.FORCE_STREAMING, L.FORCE_STREAMING | L.VARIANT_I):
             errs = _errs(case, _run_gpu(case, x, dz, p, act, flags=fl), ref)
             assert all(v <= TOL for v in errs.values()), (fl, errs)
