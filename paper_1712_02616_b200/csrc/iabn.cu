@@ -215,7 +215,7 @@ int nb_grid(const Geom& g) {
     const int64_t bytes = g.m * g.C * g.b;  // one input
     // 32 clusters of 8: resident at once (2 CTAs per SM; cudaOccupancyMaxActiveClusters
     // reports 33 on a 148-SM B200 -- 37 clusters ran a second wave of 4)
-    int64_t G = std::min<int64_t>(32 * kNbCluster, bytes / kNbStageBytes);
+    int64_t G = std::min<int64_t>(256, bytes / kNbStageBytes);
     G = std::min<int64_t>(G, g.m) / kNbCluster * kNbCluster;  // whole clusters
     return (int)(G / kNbCluster);  // records: one per cluster
 }

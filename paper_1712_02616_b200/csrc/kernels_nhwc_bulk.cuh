@@ -51,7 +51,10 @@ constexpr int kNbTrace = 8;
 // dynamic shared memory: barriers (128 B) + ring (kNbStages * kNbStageBytes); the fp64
 // epilogue reuses the ring
 constexpr size_t kNbSmem = 128 + (size_t)kNbStages * kNbStageBytes;
-constexpr int kNbCluster = 8;  // CTAs per cluster: their records are summed over DSMEM
+#ifndef IABN_NB_CLUSTER
+#define IABN_NB_CLUSTER 8
+#endif
+constexpr int kNbCluster = IABN_NB_CLUSTER;  // CTAs per cluster: records summed over DSMEM
 
 // PASS 0: F1 shifted sums (sum d, sum d^2), d = x - K.  PASS 1, V2 (default, InPlace-ABN II
 // as in the channel-resident kernels, R6): (sum dz, sum_{z<0} dz, sum dz z);
