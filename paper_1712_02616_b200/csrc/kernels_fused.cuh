@@ -296,6 +296,11 @@ __device__ __forceinline__ float lds_elem(uint32_t addr) {
 // dx = alpha dy + kappa y + cc; everything else (slabs, records, coefficients) is shared.
 template <typename T, int PASS, int MINB, bool MIS = false, int ACT = 0>
 __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedArgs a) {
+    // ACT backward with large slabs (2 CTAs/SM): the reduce warps write (y, dy) back over
+    // (z, dz) and the apply warps only combine them -- 32x256x56^2 fp32 sigmoid 76 -> 70 us;
+    // with small slabs (4 CTAs/SM) the reduce warps are the bottleneck and the apply warps
+    // invert again (the write-back measured 10-20 % slower there)
+    constexpr bool WB = ACT != 0 && PASS == 1 && MINB == 2;
     constexpr int NIN = PASS == 0 ? 1 : 2;
     constexpr int NR = PASS == 0 ? 3 : 2;  // doubles per published record
     constexpr int V = Elem<T>::kVec;
@@ -789,7 +794,9 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
 #pragma unroll
             for (int i = 0; i < NP; ++i) sn[i] = make_float2(0.f, 0.f);
             // the sums of one vector pair (z, dz) -- or of one x vector in the forward
-            auto reduce_vec = [&](const uint4 zu, const uint4 du, auto v2tag) {
+            // vv: the slot's vector index (ACT backward: y = f^-1(z) and dy = f'(z) dz are
+            // written back over z and dz, so that the apply warps do not invert again)
+            auto reduce_vec = [&](const uint4 zu, const uint4 du, auto v2tag, uint32_t vv) {
                 constexpr bool V2 = decltype(v2tag)::value;
                 if (PASS == 0) {
                     float2 d[NP];
@@ -810,6 +817,12 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         const float2 y = make_float2(Act<ACT>::inv(zz[i].x), Act<ACT>::inv(zz[i].y));
                         s1[i] = add2(s1[i], dy);
                         s2[i] = V2 ? fma2(dy, y, s2[i]) : fma2(dy, fma2(y, ig2, nb2), s2[i]);
+                        zz[i] = y;
+                        dd[i] = dy;
+                    }
+                    if constexpr (WB) {
+                        sts128(xs + vv * 16u, Pairs<T>::store(zz));
+                        sts128(ds + vv * 16u, Pairs<T>::store(dd));
                     }
                 } else if (V2 && sizeof(T) == 2) {
                     const uint32_t zw[4] = {zu.x, zu.y, zu.z, zu.w};
@@ -842,7 +855,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
             // MIS: a covering slot with elements outside the plane -- those are skipped
             // (selects, not products: the slot's other bytes may hold anything)
             auto reduce_vec_masked = [&](const uint4 zu, const uint4 du, uint32_t i, uint32_t h,
-                                         auto v2tag) {
+                                         auto v2tag, uint32_t vv) {
                 constexpr bool V2 = decltype(v2tag)::value;
                 float zz[V], dd[V];
                 unpack<T>(zu, zz);
@@ -859,9 +872,12 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     } else if constexpr (ACT != 0) {
                         // selects, not products: a masked element may be anything
                         const float dy = Act<ACT>::df(zz[k]) * dd[k];
-                        const float t2 = dy * (V2 ? Act<ACT>::inv(zz[k]) : fmaf(Act<ACT>::inv(zz[k]), ig2.x, nb2.x));
+                        const float y = Act<ACT>::inv(zz[k]);
+                        const float t2 = dy * (V2 ? y : fmaf(y, ig2.x, nb2.x));
                         *a1 += ok ? dy : 0.f;
                         *a2 += ok ? t2 : 0.f;
+                        zz[k] = y;  // written back below (masked elements: the apply skips them)
+                        dd[k] = dy;
                     } else if (V2 && sizeof(T) == 2) {
                         float* an = (k & 1) ? &sn[k >> 1].y : &sn[k >> 1].x;
                         *a1 += ok ? dd[k] : 0.f;
@@ -874,6 +890,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                                             : fmaf(dd[k] * zz[k], ig2.x, dy * nb2.x);
                         *a2 += ok ? t2 : 0.f;
                     }
+                }
+                if constexpr (WB) {
+                    sts128(xs + vv * 16u, pack<T>(zz));
+                    sts128(ds + vv * 16u, pack<T>(dd));
                 }
             };
             // all chunks of the slice; the 4-vector body issues its 8 shared loads first
@@ -890,9 +910,10 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     const uint32_t h0 = mis_plane((uint64_t)n0 * a.C + c, a.hwb).h;
                     const uint32_t dh = (uint32_t)(((uint64_t)a.C * a.hwb) & 15u);
                     const uint32_t qp = RT / W, qr = RT % W;
-                    auto one = [&](const uint4 zu, const uint4 du, uint32_t si, uint32_t sj) {
+                    auto one = [&](const uint4 zu, const uint4 du, uint32_t si, uint32_t sj,
+                                   uint32_t vv) {
                         const uint32_t h = (h0 + sj * dh) & 15u;
-                        if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) reduce_vec(zu, du, v2tag);
+                        if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) reduce_vec(zu, du, v2tag, vv);
                     };
                     // partial slots of planes [p_lo, p_hi): e = 2 (plane - p_lo) + {0 head, 1 tail}
                     auto edges = [&](uint32_t p_lo, uint32_t p_hi) {
@@ -905,7 +926,7 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                             if (si * 16u >= h && si * 16u + 16u <= h + a.hwb) continue;  // interior
                             const uint32_t v = jn * W + si;
                             const uint4 zu = lds128(xs + v * 16u);
-                            reduce_vec_masked(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, si, h, v2tag);
+                            reduce_vec_masked(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, si, h, v2tag, v);
                         }
                     };
                     for (int k = 0; k < nch; ++k) {
@@ -917,13 +938,14 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         uint32_t jn = fdiv(v, a.fd_w), i = v - jn * W;
                         for (; v + (kMRU - 1) * RT < c_hi;) {
                             uint4 zu[kMRU], du[kMRU];
-                            uint32_t iu[kMRU], ju[kMRU];
+                            uint32_t iu[kMRU], ju[kMRU], vu[kMRU];
 #pragma unroll
                             for (int q = 0; q < kMRU; ++q) {
                                 zu[q] = lds128(xs + v * 16u);
                                 du[q] = PASS == 1 ? lds128(ds + v * 16u) : zu[q];
                                 iu[q] = i;
                                 ju[q] = jn;
+                                vu[q] = v;
                                 v += RT;
                                 i += qr;
                                 jn += qp;
@@ -933,11 +955,11 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                                 }
                             }
 #pragma unroll
-                            for (int q = 0; q < kMRU; ++q) one(zu[q], du[q], iu[q], ju[q]);
+                            for (int q = 0; q < kMRU; ++q) one(zu[q], du[q], iu[q], ju[q], vu[q]);
                         }
                         for (; v < c_hi;) {
                             const uint4 zu = lds128(xs + v * 16u);
-                            one(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, i, jn);
+                            one(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, i, jn, v);
                             v += RT;
                             i += qr;
                             jn += qp;
@@ -963,11 +985,11 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                                 du[j] = PASS == 1 ? lds128(ds + (v + j * RT) * 16u) : zu[j];
                             }
     #pragma unroll
-                            for (int j = 0; j < kRU; ++j) reduce_vec(zu[j], du[j], v2tag);
+                            for (int j = 0; j < kRU; ++j) reduce_vec(zu[j], du[j], v2tag, v + j * RT);
                         }
                         for (; v < c_hi; v += RT) {
                             const uint4 zu = lds128(xs + v * 16u);
-                            reduce_vec(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, v2tag);
+                            reduce_vec(zu, PASS == 1 ? lds128(ds + v * 16u) : zu, v2tag, v);
                         }
                     }
                 }
@@ -976,6 +998,9 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                 sweep(std::true_type{});
             else
                 sweep(std::false_type{});
+            // ACT backward: the (y, dy) write-back reaches the apply warps through the record
+            // hand-off (release / acquire); the TMA refill of this buffer is ordered after it
+            if constexpr (WB) fence_proxy_async_smem();
             if (tid == 0) IABN_TRACE(a, t, 8);
             // fold the thread's fp32 chains and the warp in fp32 (a few rounding steps on
             // partial sums of at most a few thousand terms), the warps and CTAs in fp64
@@ -1065,16 +1090,17 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                         w[i] = make_float2(fmaxf(y.x, ay.x), fmaxf(y.y, ay.y));
                     }
                 }
-            } else if constexpr (ACT != 0) {  // dx = alpha f'(z) dz + kappa f^-1(z) + cc
+            } else if constexpr (ACT != 0) {  // dx = alpha dy + kappa y + cc
                 float2 dd[NP];
                 Pairs<T>::load(xu, w);
                 Pairs<T>::load(du, dd);
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
-                    const float2 dy = make_float2(Act<ACT>::df(w[i].x) * dd[i].x,
-                                                  Act<ACT>::df(w[i].y) * dd[i].y);
-                    const float2 y = make_float2(Act<ACT>::inv(w[i].x), Act<ACT>::inv(w[i].y));
-                    w[i] = fma2(make_float2(P.x, P.x), dy, fma2(make_float2(P.y, P.y), y, make_float2(mu, mu)));
+                    if constexpr (!WB) {  // else (y, dy) were written back by the reduce warps
+                        dd[i] = make_float2(Act<ACT>::df(w[i].x) * dd[i].x, Act<ACT>::df(w[i].y) * dd[i].y);
+                        w[i] = make_float2(Act<ACT>::inv(w[i].x), Act<ACT>::inv(w[i].y));
+                    }
+                    w[i] = fma2(make_float2(P.x, P.x), dd[i], fma2(make_float2(P.y, P.y), w[i], make_float2(mu, mu)));
                 }
             } else {
                 float2 dd[NP];
@@ -1129,10 +1155,11 @@ __global__ void __launch_bounds__(kFusedThreads, MINB) fused_kernel(const FusedA
                     Pairs<T>::load(du, dd);
 #pragma unroll
                     for (int j = 0; j < NP; ++j) {
-                        const float2 dy = make_float2(Act<ACT>::df(w[j].x) * dd[j].x,
-                                                      Act<ACT>::df(w[j].y) * dd[j].y);
-                        const float2 y = make_float2(Act<ACT>::inv(w[j].x), Act<ACT>::inv(w[j].y));
-                        w[j] = fma2(make_float2(P.x, P.x), dy, fma2(make_float2(P.y, P.y), y, make_float2(mu, mu)));
+                        if constexpr (!WB) {
+                            dd[j] = make_float2(Act<ACT>::df(w[j].x) * dd[j].x, Act<ACT>::df(w[j].y) * dd[j].y);
+                            w[j] = make_float2(Act<ACT>::inv(w[j].x), Act<ACT>::inv(w[j].y));
+                        }
+                        w[j] = fma2(make_float2(P.x, P.x), dd[j], fma2(make_float2(P.y, P.y), w[j], make_float2(mu, mu)));
                     }
                 } else {
                     float2 dd[NP];
