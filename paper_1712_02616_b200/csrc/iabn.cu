@@ -1313,13 +1313,35 @@ int apply_grid(int64_t E, int b, int sms) {
 
 // NHWC aligned: a grid whose stride (grid * kThreads vectors) is a multiple of the
 // C/V vectors of one row, so every thread keeps one channel group (0 = not possible)
-int nhwc_grid(const Geom& g, int64_t nvec, int sms) {
+// Resident CTAs per SM of a kernel (cached per kernel; 0 if the query fails)
+int blocks_per_sm(const void* fn) {
+    static std::mutex mu;
+    static std::pair<const void*, int> cache[64];
+    static int n = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    for (int i = 0; i < n; ++i)
+        if (cache[i].first == fn) return cache[i].second;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, 0) != cudaSuccess) b = 0;
+    cudaGetLastError();
+    if (n < 64) cache[n++] = {fn, b};
+    return b;
+}
+
+// NHWC aligned: a grid whose stride (grid * kThreads vectors) is a multiple of the C/V
+// vectors of one row, so every thread keeps one channel group (0 = not possible); one
+// batch of kNhwcApplyUnroll vectors per thread, but at most one wave of resident CTAs
+// (bpsm per SM) for the bf16 applies: r02 ncu, 784 CTAs at 444 resident ran a 77 % second
+// wave (bf16 128x56^2 forward 23.8 -> 21.1 us, 64x112^2 37.7 -> 31.4 us)
+int nhwc_grid(const Geom& g, int64_t nvec, int sms, int bpsm = 0) {
     const int64_t cv = g.C * g.b / 16;
     const int64_t q = cv / std::gcd<int64_t>(cv, kThreads);  // grid must be a multiple of q
-    // one batch of kNhwcApplyUnroll vectors per thread (later waves of CTAs start as earlier ones
-    // finish; r02: a cap of 8 CTAs per SM left threads a dependent tail)
-    const int64_t want = std::min<int64_t>((nvec + kThreads * kNhwcApplyUnroll - 1) / (kThreads * kNhwcApplyUnroll),
-                                           (int64_t)sms * 64);
+    int64_t want = std::min<int64_t>((nvec + kThreads * kNhwcApplyUnroll - 1) / (kThreads * kNhwcApplyUnroll),
+                                     (int64_t)sms * 64);
+    // (only for the register-heavy kernels, <= 3 CTAs per SM: the bf16 applies; with more
+    // resident CTAs the waves of fresh CTAs overlap better than a per-thread loop, e.g.
+    // fp32 32x256x56^2 forward 50.9 -> 55.1 us with the cap)
+    if (bpsm > 0 && bpsm <= 3 && want > (int64_t)sms * bpsm) want = (int64_t)sms * bpsm / q * q;
     if (q > (int64_t)sms * 16) return 0;
     return (int)(std::max<int64_t>(1, (want + q - 1) / q) * q);
 }
@@ -1347,7 +1369,8 @@ iabn_status launch_fwd_apply_ev(const Geom& g, const void* x, void* z, const flo
             else
                 launch_pdl(fwd_apply_kernel<T, 0, false, EV>, grid, kThreads, 0, st, xp, zp, coef, E, fh, fc, slope, ev);
         } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
-            launch_pdl(fwd_apply_nhwc_kernel<T, EV>, nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st,
+            const int bp = blocks_per_sm((const void*)fwd_apply_nhwc_kernel<T, EV>);
+            launch_pdl(fwd_apply_nhwc_kernel<T, EV>, nhwc_grid(g, E / (16 / g.b), sms, bp), kThreads, 0, st,
                 xp, zp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope, ev);
         } else {
             if (al)
@@ -1390,7 +1413,8 @@ iabn_status launch_bwd_apply(const Geom& g, const void* z, const void* dz, void*
             else
                 launch_pdl(bwd_apply_kernel<T, 0, false>, grid, kThreads, 0, st, zp, dzp, dxp, coef, E, fh, fc, slope, inv_slope);
         } else if (al && nhwc_grid(g, E / (16 / g.b), sms) > 0) {
-            launch_pdl(bwd_apply_nhwc_kernel<T>, nhwc_grid(g, E / (16 / g.b), sms), kThreads, 0, st,
+            const int bp = blocks_per_sm((const void*)bwd_apply_nhwc_kernel<T>);
+            launch_pdl(bwd_apply_nhwc_kernel<T>, nhwc_grid(g, E / (16 / g.b), sms, bp), kThreads, 0, st,
                 zp, dzp, dxp, coef, (uint32_t)(E / (16 / g.b)), (uint32_t)(g.C * g.b / 16), slope,
                 inv_slope);
         } else {
@@ -1841,7 +1865,10 @@ iabn_status act_elementwise(const Geom& g, int pass, const float* in0, const flo
         const uint32_t E = (uint32_t)(nn * g.C * g.HW);
         const int grid = apply_grid(E, 4, sms);
         const bool al = g.layout == IABN_NCHW ? g.HW % 4 == 0 : g.C % 4 == 0;
-        const int fixed = g.layout == IABN_NHWC && al ? nhwc_grid(g, E / 4, sms) : 0;
+        const int fixed = g.layout == IABN_NHWC && al
+                              ? nhwc_grid(g, E / 4, sms, blocks_per_sm(pass == 0 ? (const void*)act_apply_fixed_kernel<ACT, 0>
+                                                                                 : (const void*)act_apply_fixed_kernel<ACT, 1>))
+                              : 0;
         const float *a = in0 + off, *b = in1 ? in1 + off : nullptr;
         float* o = out + off;
 #define IABN_ACT_LAUNCH(P, LY, AL) \

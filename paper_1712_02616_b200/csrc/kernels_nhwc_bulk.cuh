@@ -27,6 +27,9 @@
 
 namespace iabn {
 
+#ifndef IABN_NB_EVICT_LAST
+#define IABN_NB_EVICT_LAST 0
+#endif
 constexpr int kNbStages = 4;
 constexpr uint32_t kNbStageBytes = 16384;  // per stage, all inputs together
 
@@ -112,6 +115,12 @@ __global__ void __launch_bounds__(kThreads, 2) nhwc_bulk_reduce_kernel(const NbA
         const int64_t r0 = (s + k * G) * (int64_t)a.rps;
         const uint32_t bytes = rows_of(k) * rowb;
         mbar_arrive_expect_tx(&full[st], bytes * NI);
+#if IABN_NB_EVICT_LAST  // experiments: keep x in L2 for the apply's re-read
+        if (PASS == 0)
+            bulk_g2s_hint(ring + (size_t)st * kNbStageBytes, src0 + r0 * rowb, bytes, &full[st],
+                          l2_policy_evict_last());
+        else
+#endif
         bulk_g2s(ring + (size_t)st * kNbStageBytes, src0 + r0 * rowb, bytes, &full[st]);
         if (NI == 2)
             bulk_g2s(ring + (size_t)st * kNbStageBytes + SB, src1 + r0 * rowb, bytes, &full[st]);
