@@ -239,3 +239,24 @@ def test_activation_names():
         F._act("relu")  # not invertible
     with pytest.raises(ValueError):
         Pk.InPlaceABN(4, activation="gelu")
+
+
+def test_nhwc_bulk_ring_plan_host_logic():
+    """The NHWC bulk-ring reduction plan (iabn_debug_nb_records, host only): records = whole
+    clusters of 8 CTAs, at most 32 (256 CTAs), >= 8 stages of 16 KB; not for rows over 4 KB,
+    NCHW, or rows that are not 16-byte aligned."""
+    f = L.lib.iabn_debug_nb_records
+    f.argtypes = [ctypes.c_void_p]
+    f.restype = ctypes.c_int
+
+    def rec(n, c, hw, dt=L.BF16, ly=L.NHWC):
+        d = L.desc(n, c, hw, dt, ly)
+        return f(ctypes.addressof(d))
+    assert rec(32, 128, 3136) == 32                 # 25.7 MB: capped at 32 clusters
+    assert rec(1, 64, 1024) == 1                    # 128 KB: 8 CTAs of one 16 KB stage
+    assert rec(4, 64, 1024) == 4                    # 512 KB: 32 CTAs
+    assert rec(1, 64, 512) == 0                     # 64 KB: 4 CTAs, no whole cluster
+    assert rec(32, 2048, 49) > 0                    # 4 KB rows: still bulk
+    assert rec(32, 2080, 49) == 0                   # > 4 KB rows
+    assert rec(32, 128, 3136, ly=L.NCHW) == 0       # NCHW: never
+    assert rec(32, 7, 3136, dt=L.F32) == 0          # 28-byte rows: not 16-byte aligned
